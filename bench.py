@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: harmonic-mean GTEPS of the hybrid BFS over 64 roots (BASELINE.json).
+
+One *step* = one Graph500 sweep: a traversal from each of the 64 sampled roots
+(harness.sample_sources, seed 1) of the configured graph.  W warm-up sweeps,
+then exactly K timed sweeps.  Per traversal the time is the device time of the
+persistent traversal kernel (init + all layers), from CUDA events on the
+launching stream; L2 is flushed (a 256 MB write) before every traversal,
+outside the events.  value = harmonic mean of m / t over all timed traversals
+(= total edges / total time).
+
+Extra keys:
+  e2e          same metric through the reference-facing call with HOST outputs
+               (hybrid_bfs-style: kernel + D2H of parent and level into pinned
+               host memory, wall clock per traversal)
+  roofline     B_sector (SURVEY §8(d) byte model, device accounting pass) per
+               traversal / kernel time vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline the reference's compiled CPU kernels (oracle/_ref) on a bounded
+               sample of roots, timed like harness._run_one
+  clocks       nvidia-smi samples taken during the timed region
+
+--impl reference runs the reference's CPU path instead (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    # name: (graph params, heuristic kwargs, reference-arm heuristic)
+    "c1": dict(scale=16, probs=(0.57, 0.19, 0.19, 0.05), heur=dict(heuristic="reference"),
+               ref=dict(alpha=1024, beta=64), label="kron_s16_ef16"),
+    "c2": dict(scale=20, probs=(0.57, 0.19, 0.19, 0.05),
+               heur=dict(heuristic="beamer", alpha=14, beta=24, counter_mode="edge"),
+               ref=dict(alpha=14, beta=24), label="kron_s20_ef16_a14b24"),
+    "c3": dict(scale=22, probs=(0.25, 0.25, 0.25, 0.25),
+               heur=dict(heuristic="beamer", alpha=14, beta=24, counter_mode="edge"),
+               ref=dict(alpha=1024, beta=64), label="uniform_2^22_2^26"),
+    "c4": dict(scale=26, probs=(0.57, 0.19, 0.19, 0.05),
+               heur=dict(heuristic="beamer", alpha=14, beta=24, counter_mode="edge"),
+               ref=dict(alpha=14, beta=24), label="kron_s26_ef16"),
+}
+DEFAULT_CONFIG = "c2"
+ROOTS = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parent-mode", choices=("minid", "any"), default="minid")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ distributed
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    for path in (os.path.join(REPO, "MEASURED_PEAKS.json"),):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+        except (OSError, KeyError, ValueError):
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profiled_traffic(label):
+    """dram bytes per launch of the traversal kernel from the committed ncu summary."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(label)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------- reference
+
+def reference_graph(cfg):
+    from oracle import oracle as O
+    from oracle import ref_runner
+
+    O.build()
+    u, v = O.generate(cfg["scale"], 16, 1, cfg["probs"])
+    h = O.csr_build(u, v, 1 << cfg["scale"])
+    del u, v
+    return h, ref_runner.RefGraph(h.row_starts, h.adjacency, h.in_edges_total)
+
+
+def reference_sample_size(cfg):
+    return {16: 64, 20: 16, 22: 4, 26: 2}.get(cfg["scale"], 4)
+
+
+def run_reference(args, cfg):
+    from oracle import oracle as O
+    from oracle import ref_runner
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    h, rg = reference_graph(cfg)
+    roots = O.sample_sources(h, ROOTS, 1)
+    k = reference_sample_size(cfg)
+    sample = roots[:k]
+    for _ in range(args.warmup):
+        ref_runner.time_roots(rg, sample[:1], **cfg["ref"])
+    secs = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s, _r = ref_runner.time_roots(rg, sample, **cfg["ref"])
+        secs += s
+    wall = time.perf_counter() - t0
+    m = h.in_edges_total
+    value = len(secs) * m / sum(secs) / 1e9
+    info = ref_runner.cpu_info()
+    line = {
+        "impl": "reference",
+        "metric": "harmonic-mean GTEPS over 64 roots",
+        "value": value, "unit": "GTEPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (reference R-MAT generator restated, seed 1)",
+        "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
+                   "roots_per_step": int(k), "mode": "simd-hybrid", **cfg["ref"]},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
+                         "sample": f"{k} of the 64 sampled roots per step, reference native "
+                                   f"kernels (hybfs._native, {info['variant']}), 1 thread",
+                         **info},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_for(cfg):
+    """Bounded reference CPU sample (about 10 s) for the N=1 line."""
+    from oracle import oracle as O
+    from oracle import ref_runner
+
+    h, rg = reference_graph(cfg)
+    roots = O.sample_sources(h, ROOTS, 1)
+    k = reference_sample_size(cfg)
+    ref_runner.time_roots(rg, roots[:1], **cfg["ref"])
+    secs, _ = ref_runner.time_roots(rg, roots[:k], **cfg["ref"])
+    value = len(secs) * h.in_edges_total / sum(secs) / 1e9
+    info = ref_runner.cpu_info()
+    return {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
+            "sample": f"{k} of the 64 sampled roots, simd-hybrid with the reference rule "
+                      f"alpha={cfg['ref']['alpha']} beta={cfg['ref']['beta']}, reference "
+                      f"native kernels ({info['variant']}), 1 thread (reference is single-threaded)",
+            **info}
+
+
+# -------------------------------------------------------------------- ours
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_1704_02259_b200 as hb
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    params = hb.GraphParams(scale=cfg["scale"], edgefactor=16, seed=1, probs=cfg["probs"])
+    g = hb.generate_graph(params)
+    roots = hb.sample_sources(g, ROOTS, 1)
+    p = hb.HeuristicParams(**cfg["heur"])
+    n, m = g.num_vertices, g.in_edges_total
+    parent = torch.empty(n, dtype=torch.int32, device=dev)
+    level = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def sweep(record):
+        times = []
+        for s in roots:
+            flush.fill_(1)
+            r = hb.bfs(g, int(s), p, use_simd=True, parent_mode=args.parent_mode, device=True,
+                       trace=record, out=(parent, level))
+            times.append(r.device_seconds)
+            if record:
+                record.append(r.trace)
+        return times
+
+    for _ in range(args.warmup):
+        sweep(None)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    per_root = [[] for _ in roots]
+    launches = 0
+    with ClockSampler(dev.index) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            tr = []
+            ts = sweep(tr)
+            for i, t in enumerate(ts):
+                per_root[i].append(t)
+            launches += len(ts)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    total_dev = sum(sum(x) for x in per_root)
+    if ws > 1:
+        t = torch.tensor([total_dev], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_dev = float(t.item())
+    traversals = len(roots) * args.steps
+    value = ws * traversals * m / total_dev / 1e9
+    ms_per_step = total_dev / args.steps * 1e3
+
+    # --- validation + byte accounting (untimed), one pass over the roots
+    invalid = 0
+    b_sector = b_useful = 0
+    t_roots = 0.0
+    for i, s in enumerate(roots):
+        r = hb.bfs(g, int(s), p, use_simd=True, parent_mode=args.parent_mode, device=True,
+                   trace=True, out=(parent, level))
+        rep = hb.validate_tree(g, int(s), parent, level, check_minid=args.parent_mode == "minid")
+        invalid += 0 if rep.ok else 1
+        bs, bu = hb.traversal_bytes(g, int(s), level, r.trace)
+        b_sector += bs
+        b_useful += bu
+        t_roots += statistics.mean(per_root[i])
+    peak, peak_src = measured_peak()
+    achieved = b_sector / t_roots / 1e9
+    traffic = profiled_traffic(cfg["label"])
+
+    # --- e2e: reference-facing call with host outputs (kernel + D2H into pinned memory)
+    hpar = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    hlev = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+    e2e_secs = []
+    for s in roots:
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        hb.bfs(g, int(s), p, use_simd=True, parent_mode=args.parent_mode, device=False,
+               trace=True, out=(hpar, hlev))
+        e2e_secs.append(time.perf_counter() - t1)
+    e2e_value = len(e2e_secs) * m / sum(e2e_secs) / 1e9
+
+    if rank != 0:
+        return 0
+    line = {
+        "metric": "harmonic-mean GTEPS over 64 roots",
+        "value": value, "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (bit-exact reference R-MAT generator on device, seed 1)",
+        "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
+                   "roots": ROOTS, "heuristic": cfg["heur"], "parent_mode": args.parent_mode,
+                   "parallelism": "replicas" if ws > 1 else "single-gpu",
+                   "l2": "flushed (256 MB write) before every traversal", "m_edges": m,
+                   "arcs": g.num_arcs, "invalid_trees": invalid},
+        "gpu_launches": launches,
+        "wall_s_timed_region": wall,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "bfs_kernel (persistent, one launch per traversal)",
+                     "bytes_per_launch": b_sector / len(roots),
+                     "useful_bytes_per_launch": b_useful / len(roots),
+                     "launch_ms": t_roots / len(roots) * 1e3, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 4 * len(roots),
+                "d2h_bytes_per_step": len(roots) * (8 * n + 256)},
+        "clocks": clk.summary(),
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_for(cfg)
+        except Exception as ex:  # the product line must still print
+            line["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+/*
+ * hbfs.h — C ABI of the B200-native hybrid BFS (libhbfs.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path (package `hybfs`
+ * 0.1.0, /root/reference/pkg/src/hybfs).  Plain pointers, sizes and status
+ * codes only; no torch or C++ types.  Every entry point names the reference
+ * interface it replaces.  Device pointers are CUDA global-memory pointers of
+ * the current device; `stream` is a cudaStream_t (NULL = legacy stream).
+ *
+ * Status codes map onto the reference's exception types (hybfs raises them in
+ * Python, its kernels never fail): 0 OK, 1 ValueError, 2 IndexError,
+ * 3 CapacityError (generator.py:32-33, csr.py:50-51), 4 CUDA error and
+ * 5 NCCL error (RuntimeError).  No C++ exception ever crosses this ABI;
+ * hbfs_last_error() returns the thread-local message of the last failure.
+ */
+#ifndef HBFS_H
+#define HBFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HBFS_OK 0
+#define HBFS_EINVAL 1
+#define HBFS_ERANGE 2
+#define HBFS_ECAPACITY 3
+#define HBFS_ECUDA 4
+#define HBFS_ENCCL 5
+
+#define HBFS_NIL 0xFFFFFFFFu /* frontier.py:16 */
+#define HBFS_UNREACHED (-1)  /* frontier.py:19 */
+
+#define HBFS_TOP_DOWN 0
+#define HBFS_BOTTOM_UP 1
+
+#define HBFS_HEURISTIC_REFERENCE 0 /* hybrid.py:62-80 (n_f vs e_u//alpha, n//beta) */
+#define HBFS_HEURISTIC_BEAMER 1    /* Beamer/GAP rule on m_f, m_u, n_f */
+
+#define HBFS_PARENT_MINID 0 /* deterministic: min-id neighbour one level up */
+#define HBFS_PARENT_ANY 1   /* first claimer wins; passes the Graph500 tree checks */
+
+typedef struct hbfs_graph hbfs_graph; /* device-resident CSR + per-root workspace */
+
+/* Traversal knobs: HeuristicParams (hybrid.py:27-44) + VecConfig (lanes.py:30-41)
+ * + hybrid_bfs(use_simd, force_direction) (hybrid.py:83-91). */
+typedef struct {
+    int32_t heuristic;       /* HBFS_HEURISTIC_* */
+    int32_t counter_mode;    /* 0 = "vertex", 1 = "edge" (hybrid.py:36-44) */
+    int64_t alpha;           /* >= 1 */
+    int64_t beta;            /* >= 1 */
+    int32_t max_pos;         /* >= 1; VecConfig.max_pos, feeds the trace counters */
+    int32_t use_simd;        /* trace "kernel" column and gathers/fallbacks */
+    int32_t force_direction; /* -1 none, HBFS_TOP_DOWN, HBFS_BOTTOM_UP */
+    int32_t parent_mode;     /* HBFS_PARENT_* */
+} hbfs_params;
+
+/* LayerTraceRow (hybrid.py:47-59); elapsed is device time of the layer. */
+typedef struct {
+    int32_t layer;
+    int32_t direction;
+    int64_t v_f, e_f, e_u, f_value, g_value;
+    int64_t fallback_count, gather_count;
+    double elapsed;
+} hbfs_layer_row;
+
+int hbfs_version(void);
+const char *hbfs_last_error(void);
+
+/* ---- graph input (L1): replaces csr.from_arrays / csr.build (csr.py:41-74) ---- */
+
+/* CSR from reference-layout arrays: row_starts int64[n+1], adjacency uint32[arcs]
+ * with rows sorted ascending (csr.py:22-23).  m_edges = in_edges_total (csr.py:73).
+ * on_device: 1 if both pointers are device pointers, 0 for host memory. */
+int hbfs_graph_from_csr(const int64_t *row_starts, const uint32_t *adjacency, int64_t n,
+                        int64_t m_edges, int on_device, void *stream, hbfs_graph **out);
+
+/* On-device CSR build from an undirected edge list u,v uint32[m] (generator.EdgeList,
+ * generator.py:85-99): both arcs per edge, rows sorted ascending; dedup=0 keeps
+ * duplicates and self-loops bit-exactly like csr.from_arrays, dedup=1 applies
+ * per-row unique + self-loop removal. */
+int hbfs_graph_build(const uint32_t *u, const uint32_t *v, int64_t m, int64_t n, int dedup,
+                     int on_device, void *stream, hbfs_graph **out);
+
+/* Device R-MAT generator, bit-exact with generator.generate (generator.py:136-159):
+ * thresholds = {a, a+b, a+b+c} as the host computes them in Python order.
+ * Writes u,v uint32[2^scale * edgefactor] (device or host pointers). */
+int hbfs_generate_edges(int scale, int64_t edgefactor, uint64_t seed, const double thresholds[3],
+                        int permute, uint32_t *u, uint32_t *v, int on_device, void *stream);
+
+/* generate + build without leaving the device. */
+int hbfs_graph_generate(int scale, int64_t edgefactor, uint64_t seed, const double thresholds[3],
+                        int permute, int dedup, void *stream, hbfs_graph **out);
+
+/* n, arcs, in_edges_total, max degree, and whether offsets are 64-bit. */
+int hbfs_graph_info(const hbfs_graph *g, int64_t *n, int64_t *arcs, int64_t *m_edges,
+                    int64_t *max_degree, int32_t *wide_offsets);
+
+/* Copy the CSR out in the reference layout (int64 row_starts, uint32 adjacency). */
+int hbfs_graph_export(const hbfs_graph *g, int64_t *row_starts, uint32_t *adjacency,
+                      int on_device, void *stream);
+
+int hbfs_graph_free(hbfs_graph *g);
+
+/* harness.sample_sources (harness.py:73-97) on device: writes `count` roots to
+ * out (host pointer).  Returns HBFS_EINVAL if too few eligible vertices. */
+int hbfs_sample_sources(const hbfs_graph *g, int64_t count, uint64_t seed, int allow_isolated,
+                        uint32_t *out);
+
+/* ---- traversal (L2-L4): replaces hybrid.hybrid_bfs (hybrid.py:83-175) and its
+ * per-layer engine.run_* dispatch (engine.py:81-155).  The whole traversal runs
+ * on device; the direction switch is decided on device from fused counters.
+ * parent: uint32[n] (NIL = unreached), level: int32[n] (-1 = unreached); either
+ * may be NULL.  on_device says where parent/level live.  trace: host array of
+ * trace_cap rows (may be NULL); *n_layers receives the total layer count.
+ * *device_ms receives the device time of init + traversal (CUDA events). */
+int hbfs_bfs(hbfs_graph *g, int64_t root, const hbfs_params *p, uint32_t *parent,
+             int32_t *level, int on_device, hbfs_layer_row *trace, int64_t trace_cap,
+             int64_t *n_layers, float *device_ms, void *stream);
+
+/* ---- validation: replaces harness.validate_tree (harness.py:129-205) ----
+ * Graph500 rules on device, in the reference's order 1, 2, 5, 3, 4, using the
+ * level array for rule 3.  *rule = 0 when valid; *witness = offending vertex.
+ * check_minid=1 additionally checks the deterministic parent rule (rule 6). */
+int hbfs_validate(hbfs_graph *g, int64_t root, const uint32_t *parent, const int32_t *level,
+                  int on_device, int check_minid, int32_t *rule, int64_t *witness, void *stream);
+
+/* ---- measurement: algorithmic bytes of one traversal ----
+ * Given the level array (device) and the direction of every layer, returns
+ * B_sector (unique 32-byte sectors) and B_useful.  Untimed accounting pass. */
+int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *level_dev,
+                         const int32_t *directions, int64_t n_layers, int64_t *b_sector,
+                         int64_t *b_useful, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HBFS_H */

@@ -1,0 +1,165 @@
+"""Device-resident CSR graph — the reference's ``hybfs.csr`` API (csr.py:18-78)
+backed by libhbfs.
+
+``build`` / ``from_arrays`` construct the CSR on the GPU (radix sort of both
+arc directions, csrc/graph.cu) bit-exactly like ``csr.from_arrays``
+(csr.py:46-74): duplicates and self-loops kept, rows ascending.  ``dedup=True``
+gives the BASELINE.json variant (per-row unique, self-loops dropped).
+``generate_graph`` runs generator + build without leaving the device.
+``from_csr`` imports any reference-layout CSR (e.g. a ``hybfs.CsrGraph``).
+Host copies of ``row_starts`` / ``adjacency`` are exported lazily.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .generator import CapacityError, EdgeList, GraphParams, thresholds
+
+
+class CsrGraph:
+    """CSR over ``num_vertices`` vertices living on the current CUDA device."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        lib = _lib.load()
+        n, arcs, m, md = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        wide = C.c_int32()
+        _lib.check(lib.hbfs_graph_info(handle, C.byref(n), C.byref(arcs), C.byref(m),
+                                       C.byref(md), C.byref(wide)))
+        self.num_vertices = int(n.value)
+        self.num_arcs = int(arcs.value)
+        self.in_edges_total = int(m.value)
+        self.max_degree = int(md.value)
+        self.wide_offsets = bool(wide.value)
+        self._rs = None
+        self._adj = None
+
+    # -- lifetime
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise RuntimeError("graph has been freed")
+        return self._h
+
+    def free(self) -> None:
+        if self._h is not None:
+            _lib.load().hbfs_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    # -- reference accessors (csr.py:25-38)
+    @property
+    def row_starts(self) -> np.ndarray:
+        if self._rs is None:
+            self._export()
+        return self._rs
+
+    @property
+    def adjacency(self) -> np.ndarray:
+        if self._adj is None:
+            self._export()
+        return self._adj
+
+    def _export(self) -> None:
+        rs = np.empty(self.num_vertices + 1, dtype=np.int64)
+        adj = np.empty(self.num_arcs, dtype=np.uint32)
+        _lib.check(_lib.load().hbfs_graph_export(self.handle, rs.ctypes.data_as(C.c_void_p),
+                                                 adj.ctypes.data_as(C.c_void_p), 0, None))
+        rs.setflags(write=False)
+        adj.setflags(write=False)
+        self._rs, self._adj = rs, adj
+
+    def degree(self, v: int) -> int:
+        if not 0 <= v < self.num_vertices:
+            raise IndexError(f"vertex {v} out of range [0, {self.num_vertices})")
+        return int(self.row_starts[v + 1] - self.row_starts[v])
+
+    def row(self, v: int) -> np.ndarray:
+        if not 0 <= v < self.num_vertices:
+            raise IndexError(f"vertex {v} out of range [0, {self.num_vertices})")
+        return self.adjacency[self.row_starts[v]: self.row_starts[v + 1]]
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.row_starts)
+
+    def __repr__(self) -> str:
+        return (f"CsrGraph(n={self.num_vertices}, arcs={self.num_arcs}, "
+                f"m={self.in_edges_total}, device)")
+
+
+def _new(fn, *args) -> CsrGraph:
+    h = C.c_void_p()
+    _lib.check(fn(*args, C.byref(h)))
+    return CsrGraph(h)
+
+
+def from_arrays(eu, ev, n: int, dedup: bool = False) -> CsrGraph:
+    """CSR from endpoint arrays (csr.py:46-74), built on the device."""
+    lib = _lib.load(require_device=True)
+    if n > 1 << 32:
+        raise CapacityError("vertex ids are 32-bit; at most 2^32 vertices")
+    eu = np.ascontiguousarray(eu, dtype=np.uint32)
+    ev = np.ascontiguousarray(ev, dtype=np.uint32)
+    if len(eu) != len(ev):
+        raise ValueError("endpoint arrays differ in length")
+    if len(eu) and (int(eu.max()) >= n or int(ev.max()) >= n):
+        raise ValueError("endpoint id out of range")
+    return _new(lib.hbfs_graph_build, eu.ctypes.data_as(C.c_void_p), ev.ctypes.data_as(C.c_void_p),
+                len(eu), n, int(dedup), 0, None)
+
+
+def build(edges: EdgeList, dedup: bool = False) -> CsrGraph:
+    """CSR from an EdgeList (csr.py:41-43)."""
+    return from_arrays(edges.u, edges.v, edges.num_vertices, dedup=dedup)
+
+
+def generate_graph(params: GraphParams, dedup: bool = False) -> CsrGraph:
+    """generate + build entirely on the device (no host edge list)."""
+    lib = _lib.load(require_device=True)
+    if params.scale > 32:
+        raise CapacityError("vertex ids are 32-bit")
+    thr = thresholds(params.probs)
+    return _new(lib.hbfs_graph_generate, params.scale, params.edgefactor,
+                params.seed & 0xFFFFFFFFFFFFFFFF, thr.ctypes.data_as(C.c_void_p),
+                int(params.permute_labels), int(dedup), None)
+
+
+def from_csr(row_starts, adjacency, in_edges_total: int | None = None) -> CsrGraph:
+    """Import a reference-layout CSR (int64 row_starts, uint32 adjacency)."""
+    lib = _lib.load(require_device=True)
+    rs = np.ascontiguousarray(row_starts, dtype=np.int64)
+    adj = np.ascontiguousarray(adjacency, dtype=np.uint32)
+    n = len(rs) - 1
+    if n < 0 or int(rs[-1]) != len(adj):
+        raise ValueError("row_starts[-1] must equal len(adjacency)")
+    m = len(adj) // 2 if in_edges_total is None else int(in_edges_total)
+    return _new(lib.hbfs_graph_from_csr, rs.ctypes.data_as(C.c_void_p),
+                adj.ctypes.data_as(C.c_void_p), n, m, 0, None)
+
+
+def as_device_graph(g) -> CsrGraph:
+    """Accept our CsrGraph or any object with the reference CsrGraph fields."""
+    if isinstance(g, CsrGraph):
+        return g
+    cache = _IMPORTED.get(id(g))
+    if cache is not None and cache[0] is g:
+        return cache[1]
+    dg = from_csr(g.row_starts, g.adjacency, getattr(g, "in_edges_total", None))
+    _IMPORTED[id(g)] = (g, dg)
+    return dg
+
+
+_IMPORTED: dict = {}
+
+
+def degree(g: CsrGraph, v: int) -> int:
+    return g.degree(v)

@@ -1,0 +1,107 @@
+// Shared internals of libhbfs.so: error plumbing, the graph object, small
+// device helpers.  Nothing here is part of the C ABI (see include/hbfs.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/hbfs.h"
+
+namespace hbfs {
+
+int set_error(int code, const char *fmt, ...);
+void clear_error();
+
+#define HB_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return ::hbfs::set_error(HBFS_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, \
+                                     cudaGetErrorString(e_));                           \
+    } while (0)
+
+#define HB_CHECK(expr)                    \
+    do {                                  \
+        int rc_ = (expr);                 \
+        if (rc_ != HBFS_OK) return rc_;   \
+    } while (0)
+
+// Guard every C entry point: no C++ exception may cross the ABI.
+#define HB_ENTRY_BEGIN try {
+#define HB_ENTRY_END                                                           \
+    }                                                                          \
+    catch (const std::exception &ex) {                                         \
+        return ::hbfs::set_error(HBFS_ECUDA, "internal error: %s", ex.what()); \
+    }                                                                          \
+    catch (...) {                                                              \
+        return ::hbfs::set_error(HBFS_ECUDA, "internal error");                \
+    }
+
+constexpr int kBlock = 512;  // threads per CTA for the traversal kernels
+
+struct Workspace;
+
+// Device block allocation helper (owned, freed in destructor).
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    int alloc(size_t b) {
+        release();
+        if (b == 0) b = 16;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return set_error(HBFS_ECAPACITY, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
+        }
+        bytes = b;
+        return HBFS_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+}  // namespace hbfs
+
+struct hbfs_graph {
+    int64_t n = 0;
+    int64_t nw = 0;        // bitmap words ceil(n/32)
+    int64_t arcs = 0;
+    int64_t m_edges = 0;   // TEPS denominator (csr.py:73)
+    int64_t max_degree = 0;
+    int wide = 0;          // 1: 64-bit offsets (arcs >= 2^32), else 32-bit
+    int device = 0;
+    hbfs::DevBuf rs;       // OffT[n+1]
+    hbfs::DevBuf adj;      // uint32[arcs + 8] (padded for aligned uint4 reads)
+    hbfs::DevBuf posw;     // uint32[nw]: bit v = deg(v) > 0 (engine.py:29-57 `posw`)
+    hbfs::Workspace *ws = nullptr;
+    ~hbfs_graph();
+};
+
+namespace hbfs {
+
+// Narrow/widen row starts and derive per-graph metadata (posw, max degree).
+int graph_finalize(hbfs_graph *g, cudaStream_t st);
+
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+}  // namespace hbfs

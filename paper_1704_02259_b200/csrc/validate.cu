@@ -1,0 +1,457 @@
+// Device-side BFS-tree validation and algorithmic-byte accounting.
+//
+// hbfs_validate replaces harness.validate_tree (harness.py:129-205): the
+// Graph500 rules in the reference's order 1, 2, 5, 3, 4, each reporting the
+// lowest offending vertex like the reference's flatnonzero()[0].  Rule 5 uses an
+// independent level-synchronous reachability sweep (not the hybrid kernel);
+// rule 3 derives levels by pointer jumping on the parent array (the device
+// analogue of _levels_from_parents, harness.py:100-126).  Extra checks:
+// rule 6 = the deterministic min-id parent rule, rule 7 = the
+// returned level array differs from the parent-walk levels.
+//
+// hbfs_traversal_bytes computes B_sector / B_useful of SURVEY §8(d) from the
+// level array and the per-layer directions (untimed accounting pass).
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace hbfs {
+
+static inline int vgrid(int64_t items, int block = 256) {
+    int64_t g = (items + block - 1) / block;
+    if (g > 148 * 64) g = 148 * 64;
+    return (int)(g < 1 ? 1 : g);
+}
+
+#define GSTRIDE(i, N) \
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (N); i += (int64_t)gridDim.x * blockDim.x)
+
+template <typename OffT>
+__global__ void k_rule2(int64_t n, int64_t root, const OffT *rs, const uint32_t *adj,
+                        const uint32_t *parent, unsigned long long *wit) {
+    GSTRIDE(v, n) {
+        const uint32_t p = parent[v];
+        if (p == HBFS_NIL || v == root) continue;
+        uint64_t lo = rs[v], hi = rs[v + 1];
+        const uint64_t end = hi;
+        while (lo < hi) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (adj[mid] < p) lo = mid + 1; else hi = mid;
+        }
+        if (lo >= end || adj[lo] != p) atomicMin(wit, (unsigned long long)v);
+    }
+}
+
+// Level-synchronous reachability sweep (queue based), independent of the hybrid kernel.
+template <typename OffT>
+__global__ void k_reach_step(const uint32_t *q, int64_t qn, const OffT *rs, const uint32_t *adj,
+                             uint32_t *seen, uint32_t *nq, unsigned long long *nqn) {
+    // one warp per frontier vertex, lanes stride the row
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t u = q[i];
+        for (uint64_t k = rs[u] + lane; k < (uint64_t)rs[u + 1]; k += 32) {
+            const uint32_t w = adj[k];
+            const uint32_t b = 1u << (w & 31);
+            if (!(seen[w >> 5] & b)) {
+                const uint32_t old = atomicOr(&seen[w >> 5], b);
+                if (!(old & b)) nq[atomicAdd(nqn, 1ull)] = w;
+            }
+        }
+    }
+}
+
+__global__ void k_rule5(int64_t n, const uint32_t *parent, const uint32_t *seen,
+                        unsigned long long *wit) {
+    GSTRIDE(v, n) {
+        const bool vis = parent[v] != HBFS_NIL;
+        const bool reach = (seen[v >> 5] >> (v & 31)) & 1u;
+        if (vis != reach) atomicMin(wit, (unsigned long long)v);
+    }
+}
+
+// pointer jumping: anc/dist -> anc2/dist2
+__global__ void k_jump_init(int64_t n, int64_t root, const uint32_t *parent, uint32_t *anc,
+                            int32_t *dist) {
+    GSTRIDE(v, n) {
+        const uint32_t p = parent[v];
+        if (v == root) { anc[v] = (uint32_t)root; dist[v] = 0; }
+        else if (p == HBFS_NIL || p >= n) { anc[v] = HBFS_NIL; dist[v] = 0; }
+        else { anc[v] = p; dist[v] = 1; }
+    }
+}
+
+__global__ void k_jump(int64_t n, const uint32_t *anc, const int32_t *dist, uint32_t *anc2,
+                       int32_t *dist2) {
+    GSTRIDE(v, n) {
+        const uint32_t a = anc[v];
+        if (a == HBFS_NIL) { anc2[v] = HBFS_NIL; dist2[v] = dist[v]; continue; }
+        const uint32_t aa = anc[a];
+        anc2[v] = aa;
+        // once a chain reaches the root it stays there with dist[root] == 0
+        dist2[v] = (aa == HBFS_NIL) ? dist[v] : dist[v] + dist[a];
+        if (aa == HBFS_NIL) anc2[v] = HBFS_NIL;
+    }
+}
+
+__global__ void k_rule3(int64_t n, int64_t root, const uint32_t *parent, const uint32_t *anc,
+                        const int32_t *dist, int32_t *plev, unsigned long long *wit) {
+    GSTRIDE(v, n) {
+        const bool vis = parent[v] != HBFS_NIL;
+        const bool ok = anc[v] == (uint32_t)root;
+        plev[v] = (vis && ok) ? dist[v] : -1;
+        if (vis && !ok) atomicMin(wit, (unsigned long long)v);
+    }
+}
+
+template <typename OffT>
+__global__ void k_rule4(int64_t n, const OffT *rs, const uint32_t *adj, const int32_t *plev,
+                        const uint32_t *parent, unsigned long long *wit) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+         u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (parent[u] == HBFS_NIL) continue;
+        const int32_t lu = plev[u];
+        bool bad = false;
+        for (uint64_t k = rs[u] + lane; k < (uint64_t)rs[u + 1]; k += 32) {
+            const uint32_t w = adj[k];
+            if (parent[w] == HBFS_NIL) continue;
+            const int32_t d = lu - plev[w];
+            if (d > 1 || d < -1) bad = true;
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(wit, (unsigned long long)u);
+    }
+}
+
+template <typename OffT>
+__global__ void k_rule6(int64_t n, int64_t root, const OffT *rs, const uint32_t *adj,
+                        const int32_t *plev, const uint32_t *parent, unsigned long long *wit) {
+    GSTRIDE(v, n) {
+        const uint32_t p = parent[v];
+        if (p == HBFS_NIL || v == root) continue;
+        const int32_t want = plev[v] - 1;
+        uint32_t best = HBFS_NIL;
+        for (uint64_t k = rs[v]; k < (uint64_t)rs[v + 1]; ++k) {
+            const uint32_t w = adj[k];
+            if (plev[w] == want) { best = w; break; }  // rows ascending: first = min id
+        }
+        if (best != p) atomicMin(wit, (unsigned long long)v);
+    }
+}
+
+__global__ void k_rule7(int64_t n, const int32_t *plev, const int32_t *level,
+                        unsigned long long *wit) {
+    GSTRIDE(v, n) {
+        if (plev[v] != level[v]) atomicMin(wit, (unsigned long long)v);
+    }
+}
+
+struct Probe {
+    unsigned long long *wit = nullptr;
+    int reset(cudaStream_t st) {
+        HB_CUDA(cudaMemsetAsync(wit, 0xFF, 8, st));
+        return HBFS_OK;
+    }
+    int read(cudaStream_t st, int64_t *out) {
+        unsigned long long h = 0;
+        HB_CUDA(cudaMemcpyAsync(&h, wit, 8, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        *out = h == ~0ull ? -1 : (int64_t)h;
+        return HBFS_OK;
+    }
+};
+
+template <typename OffT>
+static int validate_impl(hbfs_graph *g, int64_t root, const uint32_t *parent, const int32_t *level,
+                         int check_minid, int32_t *rule, int64_t *witness, cudaStream_t st) {
+    const int64_t n = g->n, nw = g->nw;
+    const OffT *rs = g->rs.as<OffT>();
+    const uint32_t *adj = g->adj.as<uint32_t>();
+    DevBuf wbuf;
+    HB_CHECK(wbuf.alloc(8));
+    Probe P;
+    P.wit = wbuf.as<unsigned long long>();
+    int64_t w = -1;
+    *rule = 0;
+    *witness = -1;
+    // rule 1
+    uint32_t pr = 0;
+    HB_CUDA(cudaMemcpyAsync(&pr, parent + root, 4, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (pr != (uint32_t)root) { *rule = 1; *witness = root; return HBFS_OK; }
+    // rule 2
+    HB_CHECK(P.reset(st));
+    k_rule2<OffT><<<vgrid(n), 256, 0, st>>>(n, root, rs, adj, parent, P.wit);
+    HB_CUDA(cudaGetLastError());
+    HB_CHECK(P.read(st, &w));
+    if (w >= 0) { *rule = 2; *witness = w; return HBFS_OK; }
+    // rule 5: reachability sweep
+    {
+        DevBuf seen, qa, qb, cnt;
+        HB_CHECK(seen.alloc(nw * 4 + 16));
+        HB_CHECK(qa.alloc(n * 4 + 16));
+        HB_CHECK(qb.alloc(n * 4 + 16));
+        HB_CHECK(cnt.alloc(8));
+        HB_CUDA(cudaMemsetAsync(seen.p, 0, nw * 4 + 16, st));
+        const uint32_t r32 = (uint32_t)root, rb = 1u << (root & 31);
+        HB_CUDA(cudaMemcpyAsync(qa.p, &r32, 4, cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemcpyAsync(seen.as<uint32_t>() + (root >> 5), &rb, 4, cudaMemcpyHostToDevice, st));
+        int64_t qn = 1;
+        uint32_t *q = qa.as<uint32_t>(), *nq = qb.as<uint32_t>();
+        while (qn > 0) {
+            HB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+            k_reach_step<OffT><<<vgrid(qn * 32), 256, 0, st>>>(q, qn, rs, adj, seen.as<uint32_t>(), nq,
+                                                              cnt.as<unsigned long long>());
+            HB_CUDA(cudaGetLastError());
+            unsigned long long h = 0;
+            HB_CUDA(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+            qn = (int64_t)h;
+            std::swap(q, nq);
+        }
+        HB_CHECK(P.reset(st));
+        k_rule5<<<vgrid(n), 256, 0, st>>>(n, parent, seen.as<uint32_t>(), P.wit);
+        HB_CUDA(cudaGetLastError());
+        HB_CHECK(P.read(st, &w));
+        if (w >= 0) { *rule = 5; *witness = w; return HBFS_OK; }
+    }
+    // rule 3: parent-walk levels by pointer jumping
+    DevBuf a0, a1, d0, d1;
+    HB_CHECK(a0.alloc(n * 4 + 16));
+    HB_CHECK(a1.alloc(n * 4 + 16));
+    HB_CHECK(d0.alloc(n * 4 + 16));
+    HB_CHECK(d1.alloc(n * 4 + 16));
+    k_jump_init<<<vgrid(n), 256, 0, st>>>(n, root, parent, a0.as<uint32_t>(), d0.as<int32_t>());
+    HB_CUDA(cudaGetLastError());
+    uint32_t *anc = a0.as<uint32_t>(), *anc2 = a1.as<uint32_t>();
+    int32_t *dist = d0.as<int32_t>(), *dist2 = d1.as<int32_t>();
+    for (int64_t span = 1; span < n + 1; span <<= 1) {
+        k_jump<<<vgrid(n), 256, 0, st>>>(n, anc, dist, anc2, dist2);
+        HB_CUDA(cudaGetLastError());
+        std::swap(anc, anc2);
+        std::swap(dist, dist2);
+    }
+    int32_t *plev = dist2;  // reuse the spare buffer for the levels
+    HB_CHECK(P.reset(st));
+    k_rule3<<<vgrid(n), 256, 0, st>>>(n, root, parent, anc, dist, plev, P.wit);
+    HB_CUDA(cudaGetLastError());
+    HB_CHECK(P.read(st, &w));
+    if (w >= 0) { *rule = 3; *witness = w; return HBFS_OK; }
+    // rule 4
+    HB_CHECK(P.reset(st));
+    k_rule4<OffT><<<vgrid(n * 32), 256, 0, st>>>(n, rs, adj, plev, parent, P.wit);
+    HB_CUDA(cudaGetLastError());
+    HB_CHECK(P.read(st, &w));
+    if (w >= 0) { *rule = 4; *witness = w; return HBFS_OK; }
+    if (check_minid) {
+        HB_CHECK(P.reset(st));
+        k_rule6<OffT><<<vgrid(n), 256, 0, st>>>(n, root, rs, adj, plev, parent, P.wit);
+        HB_CUDA(cudaGetLastError());
+        HB_CHECK(P.read(st, &w));
+        if (w >= 0) { *rule = 6; *witness = w; return HBFS_OK; }
+    }
+    if (level) {
+        HB_CHECK(P.reset(st));
+        k_rule7<<<vgrid(n), 256, 0, st>>>(n, plev, level, P.wit);
+        HB_CUDA(cudaGetLastError());
+        HB_CHECK(P.read(st, &w));
+        if (w >= 0) { *rule = 7; *witness = w; return HBFS_OK; }
+    }
+    return HBFS_OK;
+}
+
+// --------------------------------------------------------- byte accounting
+
+__device__ __forceinline__ void mark(uint32_t *flags, uint64_t sector) {
+    const uint32_t b = 1u << (sector & 31);
+    uint32_t *p = flags + (sector >> 5);
+    if (!(*p & b)) atomicOr(p, b);
+}
+
+// TD layer: F = level d.  Marks rs sectors, adjacency-row sectors and visited-
+// bitmap sectors probed; counts arcs (m_f).
+template <typename OffT>
+__global__ void k_acc_td(int64_t n, int32_t d, const int32_t *level, const OffT *rs,
+                         const uint32_t *adj, int rs_bytes, uint32_t *f_rs, uint32_t *f_adj,
+                         uint32_t *f_bm, unsigned long long *cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+         u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (level[u] != d) continue;
+        const uint64_t s = rs[u], e = rs[u + 1];
+        if (lane == 0) {
+            mark(f_rs, (uint64_t)u * rs_bytes / 32);
+            mark(f_rs, (uint64_t)(u + 1) * rs_bytes / 32);
+            atomicAdd(&cnt[0], 1ull);
+            atomicAdd(&cnt[1], (unsigned long long)(e - s));
+        }
+        for (uint64_t k = s + lane; k < e; k += 32) {
+            mark(f_adj, k * 4 / 32);
+            const uint32_t w = adj[k];
+            mark(f_bm, (uint64_t)(w >> 5) * 4 / 32);
+        }
+    }
+}
+
+// BU layer: U = unvisited before the layer with deg > 0; probes(v) = 1 + first
+// position of a depth-d neighbour if v is found (level d+1), else deg(v).
+template <typename OffT>
+__global__ void k_acc_bu(int64_t n, int32_t d, const int32_t *level, const OffT *rs,
+                         const uint32_t *adj, int rs_bytes, uint32_t *f_rs, uint32_t *f_adj,
+                         uint32_t *f_bm, unsigned long long *cnt) {
+    GSTRIDE(v, n) {
+        const int32_t lv = level[v];
+        if (!(lv == -1 || lv > d)) continue;
+        const uint64_t s = rs[v], e = rs[v + 1];
+        atomicAdd(&cnt[0], 1ull);  // |U|
+        if (e == s) continue;
+        mark(f_rs, (uint64_t)v * rs_bytes / 32);
+        mark(f_rs, (uint64_t)(v + 1) * rs_bytes / 32);
+        uint64_t probes = e - s;
+        if (lv == d + 1) {
+            for (uint64_t k = s; k < e; ++k) {
+                if (level[adj[k]] == d) { probes = k - s + 1; break; }
+            }
+        }
+        atomicAdd(&cnt[1], (unsigned long long)probes);
+        uint64_t last = ~0ull;
+        for (uint64_t k = s; k < s + probes; ++k) {
+            const uint64_t sec = k * 4 / 32;
+            if (sec != last) { mark(f_adj, sec); last = sec; }
+            mark(f_bm, (uint64_t)(adj[k] >> 5) * 4 / 32);
+        }
+    }
+}
+
+// N = level d+1: parent/level sectors (4 B each) and count.
+__global__ void k_acc_new(int64_t n, int32_t d, const int32_t *level, uint32_t *f_pl,
+                          unsigned long long *cnt) {
+    GSTRIDE(v, n) {
+        if (level[v] == d + 1) {
+            mark(f_pl, (uint64_t)v * 4 / 32);
+            atomicAdd(&cnt[2], 1ull);
+        }
+    }
+}
+
+__global__ void k_popc(const uint32_t *f, int64_t words, unsigned long long *out) {
+    unsigned long long s = 0;
+    GSTRIDE(i, words) s += __popc(f[i]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+template <typename OffT>
+static int bytes_impl(hbfs_graph *g, int64_t root, const int32_t *level,
+                      const int32_t *dirs, int64_t n_layers, int64_t *b_sector, int64_t *b_useful,
+                      cudaStream_t st) {
+    const int64_t n = g->n, nw = g->nw, arcs = g->arcs;
+    const int rs_bytes = sizeof(OffT);
+    const OffT *rs = g->rs.as<OffT>();
+    const uint32_t *adj = g->adj.as<uint32_t>();
+    auto words_for = [](int64_t bytes) { return (bytes / 32 + 1 + 31) / 32 + 1; };
+    const int64_t w_rs = words_for((n + 1) * rs_bytes), w_adj = words_for(arcs * 4 + 32),
+                  w_bm = words_for(nw * 4 + 32), w_pl = words_for(n * 4 + 32);
+    DevBuf f_rs, f_adj, f_bm, f_pl, cnt, pc;
+    HB_CHECK(f_rs.alloc(w_rs * 4));
+    HB_CHECK(f_adj.alloc(w_adj * 4));
+    HB_CHECK(f_bm.alloc(w_bm * 4));
+    HB_CHECK(f_pl.alloc(w_pl * 4));
+    HB_CHECK(cnt.alloc(8 * 4));
+    HB_CHECK(pc.alloc(8 * 4));
+    const int64_t W = nw;
+    auto sec = [](int64_t bytes) { return (bytes + 31) / 32 * 32; };
+    int64_t bs = 8 * n + 12 * W;  // B_init: parent + level + 3 bitmaps
+    int64_t bu = 8 * n + 12 * W;
+    for (int64_t L = 0; L < n_layers; ++L) {
+        const int32_t d = (int32_t)L;
+        HB_CUDA(cudaMemsetAsync(f_rs.p, 0, w_rs * 4, st));
+        HB_CUDA(cudaMemsetAsync(f_adj.p, 0, w_adj * 4, st));
+        HB_CUDA(cudaMemsetAsync(f_bm.p, 0, w_bm * 4, st));
+        HB_CUDA(cudaMemsetAsync(f_pl.p, 0, w_pl * 4, st));
+        HB_CUDA(cudaMemsetAsync(cnt.p, 0, 32, st));
+        HB_CUDA(cudaMemsetAsync(pc.p, 0, 32, st));
+        unsigned long long *c = cnt.as<unsigned long long>();
+        if (dirs[L] == HBFS_TOP_DOWN)
+            k_acc_td<OffT><<<vgrid(n * 32), 256, 0, st>>>(n, d, level, rs, adj, rs_bytes, f_rs.as<uint32_t>(),
+                                                         f_adj.as<uint32_t>(), f_bm.as<uint32_t>(), c);
+        else
+            k_acc_bu<OffT><<<vgrid(n), 256, 0, st>>>(n, d, level, rs, adj, rs_bytes, f_rs.as<uint32_t>(),
+                                                    f_adj.as<uint32_t>(), f_bm.as<uint32_t>(), c);
+        HB_CUDA(cudaGetLastError());
+        k_acc_new<<<vgrid(n), 256, 0, st>>>(n, d, level, f_pl.as<uint32_t>(), c);
+        HB_CUDA(cudaGetLastError());
+        unsigned long long *p = pc.as<unsigned long long>();
+        k_popc<<<vgrid(w_rs), 256, 0, st>>>(f_rs.as<uint32_t>(), w_rs, p + 0);
+        k_popc<<<vgrid(w_adj), 256, 0, st>>>(f_adj.as<uint32_t>(), w_adj, p + 1);
+        k_popc<<<vgrid(w_bm), 256, 0, st>>>(f_bm.as<uint32_t>(), w_bm, p + 2);
+        k_popc<<<vgrid(w_pl), 256, 0, st>>>(f_pl.as<uint32_t>(), w_pl, p + 3);
+        HB_CUDA(cudaGetLastError());
+        unsigned long long hc[4], hp[4];
+        HB_CUDA(cudaMemcpyAsync(hc, cnt.p, 32, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(hp, pc.p, 32, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        // parent[N] and level[N] have identical sector sets (both 4 B per vertex)
+        const int64_t s_rs = hp[0] * 32, s_adj = hp[1] * 32, s_bm = hp[2] * 32, s_pl = 2 * hp[3] * 32;
+        const int64_t N = (int64_t)hc[2];
+        if (dirs[L] == HBFS_TOP_DOWN) {
+            const int64_t F = (int64_t)hc[0], mf = (int64_t)hc[1];
+            bs += sec(4 * F) + s_rs + s_adj + s_bm + s_pl + sec(4 * N);
+            bu += 20 * F + 4 * mf + 12 * N;
+        } else {
+            const int64_t U = (int64_t)hc[0], probes = (int64_t)hc[1];
+            bs += 4 * W + s_rs + s_adj + s_bm + s_pl + 4 * W;
+            bu += 8 * W + 8 * U + 4 * probes + 8 * N;
+        }
+    }
+    *b_sector = bs;
+    *b_useful = bu;
+    return HBFS_OK;
+}
+
+}  // namespace hbfs
+
+using namespace hbfs;
+
+extern "C" int hbfs_validate(hbfs_graph *g, int64_t root, const uint32_t *parent,
+                             const int32_t *level, int on_device, int check_minid, int32_t *rule,
+                             int64_t *witness, void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!g || !parent || !rule || !witness) return set_error(HBFS_EINVAL, "bad arguments");
+    if (root < 0 || root >= g->n) return set_error(HBFS_ERANGE, "source out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t *dp = parent;
+    const int32_t *dl = level;
+    DevBuf bp, bl;
+    if (!on_device) {
+        HB_CHECK(bp.alloc(g->n * 4 + 16));
+        HB_CUDA(cudaMemcpyAsync(bp.p, parent, g->n * 4, cudaMemcpyHostToDevice, st));
+        dp = bp.as<uint32_t>();
+        if (level) {
+            HB_CHECK(bl.alloc(g->n * 4 + 16));
+            HB_CUDA(cudaMemcpyAsync(bl.p, level, g->n * 4, cudaMemcpyHostToDevice, st));
+            dl = bl.as<int32_t>();
+        }
+    }
+    if (g->wide) return validate_impl<uint64_t>(g, root, dp, dl, check_minid, rule, witness, st);
+    return validate_impl<uint32_t>(g, root, dp, dl, check_minid, rule, witness, st);
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *level_dev,
+                                    const int32_t *directions, int64_t n_layers, int64_t *b_sector,
+                                    int64_t *b_useful, void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!g || !level_dev || !directions || !b_sector || !b_useful)
+        return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (g->wide)
+        return bytes_impl<uint64_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful, st);
+    return bytes_impl<uint32_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful, st);
+    HB_ENTRY_END
+}

@@ -1,0 +1,174 @@
+"""Edge cases the reference tests (by-hand graphs) on the CUDA path, checked
+against the pinned oracle: empty graph, isolated root, self-loops, duplicates,
+n not a multiple of 32, MAX_POS boundary, very deep graphs (multi-launch
+resume), forced directions, out-of-range roots and validator fault injection."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def graph(hb, pairs, n, dedup=False):
+    eu = np.array([p[0] for p in pairs], dtype=np.uint32)
+    ev = np.array([p[1] for p in pairs], dtype=np.uint32)
+    return hb.from_arrays(eu, ev, n, dedup=dedup), eu, ev
+
+
+def check_all(hb, oracle, pairs, n, roots=None, **kw):
+    g, eu, ev = graph(hb, pairs, n)
+    host = oracle.csr_build(eu, ev, n)
+    assert np.array_equal(g.row_starts, host.row_starts)
+    assert np.array_equal(g.adjacency, host.adjacency)
+    for s in (roots if roots is not None else range(n)):
+        for simd in (False, True):
+            for force in (None, "top-down", "bottom-up"):
+                r = hb.bfs(g, s, use_simd=simd, force_direction=force, device=False, **kw)
+                par, lev, rows = oracle.hybrid_bfs(host, s, use_simd=simd, force_direction=force)
+                assert np.array_equal(r.level, lev), (s, simd, force)
+                assert np.array_equal(r.parent, par), (s, simd, force)
+                assert len(r.trace) == len(rows)
+                for a, b in zip(r.trace, rows):
+                    assert (a.v_f, a.e_f, a.e_u, a.f_value, a.g_value, a.fallback_count,
+                            a.gather_count) == (b["v_f"], b["e_f"], b["e_u"], b["f_value"],
+                                                b["g_value"], b["fallback_count"], b["gather_count"])
+    return g
+
+
+def test_csr_by_hand(cuda):
+    hb = cuda
+    g, _, _ = graph(hb, [(0, 1), (1, 2)], 3)
+    assert list(g.row_starts) == [0, 1, 3, 4] and list(g.adjacency) == [1, 0, 2, 1]
+    g, _, _ = graph(hb, [(0, 0)], 2)
+    assert list(g.row_starts) == [0, 2, 2] and list(g.adjacency) == [0, 0]
+    g, _, _ = graph(hb, [(0, 1), (0, 1)], 2)
+    assert list(g.adjacency) == [1, 1, 0, 0] and g.num_arcs == 4
+    gd, _, _ = graph(hb, [(0, 1), (0, 1), (2, 2), (1, 0)], 3, dedup=True)
+    assert list(gd.row_starts) == [0, 1, 2, 2] and list(gd.adjacency) == [1, 0]
+    ge, _, _ = graph(hb, [], 4)
+    assert list(ge.row_starts) == [0, 0, 0, 0, 0] and ge.num_arcs == 0 and ge.in_edges_total == 0
+
+
+def test_empty_and_isolated(cuda, oracle):
+    hb = cuda
+    check_all(hb, oracle, [], 4)
+    check_all(hb, oracle, [(0, 1)], 3)  # vertex 2 isolated
+
+
+def test_small_shapes(cuda, oracle):
+    hb = cuda
+    check_all(hb, oracle, [(0, 1), (1, 2)], 3)
+    check_all(hb, oracle, [(0, 1), (1, 2), (0, 2)], 3)
+    check_all(hb, oracle, [(0, i) for i in range(1, 5)], 5)
+    check_all(hb, oracle, [(0, 0), (0, 1), (0, 1), (1, 1), (2, 3)], 37)  # n % 32 != 0
+    rng = np.random.default_rng(5)
+    pairs = [tuple(int(x) for x in rng.integers(0, 77, 2)) for _ in range(300)]
+    check_all(hb, oracle, pairs, 77, roots=range(0, 77, 7))
+
+
+def test_max_pos_boundary(cuda, oracle):
+    # test_acceptance.py:280-321 — vertex 1's only frontier neighbour at position 9
+    hb = cuda
+    pairs = [(1, v) for v in range(2, 12)]
+    g, eu, ev = graph(hb, pairs, 32)
+    host = oracle.csr_build(eu, ev, 32)
+    for max_pos in (8, 10, 12):
+        cfg = hb.VecConfig(max_pos=max_pos)
+        r = hb.bfs(g, 11, cfg=cfg, use_simd=True, force_direction="bottom-up", device=False)
+        par, lev, rows = oracle.hybrid_bfs(host, 11, use_simd=True, force_direction="bottom-up",
+                                           max_pos=max_pos)
+        assert r.parent[1] == 11 and np.array_equal(r.parent, par)
+        assert r.trace[0].fallback_count == rows[0]["fallback_count"]
+        assert (r.trace[0].fallback_count >= 1) == (max_pos == 8)
+
+
+def test_high_degree_hub_long_rows(cuda, oracle):
+    # rows far longer than the per-lane probes: warp-cooperative scan + TD chunking
+    hb = cuda
+    n = 5000
+    pairs = [(0, v) for v in range(1, n)] + [(v, v + 1) for v in range(1, n - 1)]
+    pairs += [(4999, v) for v in range(2, 3000, 3)]
+    check_all(hb, oracle, pairs, n, roots=[0, 1, 2500, 4999])
+
+
+def test_deep_path_resumes_across_launches(cuda, oracle):
+    # 3000 layers > the per-launch trace capacity: exercises the persisted state
+    hb = cuda
+    n = 3000
+    pairs = [(i, i + 1) for i in range(n - 1)]
+    g, eu, ev = graph(hb, pairs, n)
+    host = oracle.csr_build(eu, ev, n)
+    r = hb.bfs(g, 0, use_simd=True, device=False)
+    par, lev, rows = oracle.hybrid_bfs(host, 0, use_simd=True)
+    assert len(r.trace) == len(rows) == n
+    assert np.array_equal(r.level, lev) and np.array_equal(r.parent, par)
+    assert [t.direction == "bottom-up" for t in r.trace] == [bool(x["direction"]) for x in rows]
+
+
+def test_errors(cuda):
+    hb = cuda
+    g, _, _ = graph(hb, [(0, 1), (1, 2)], 3)
+    with pytest.raises(IndexError):
+        hb.bfs(g, 3)
+    with pytest.raises(IndexError):
+        hb.hybrid_bfs(g, -1)
+    with pytest.raises(ValueError):
+        hb.sample_sources(g, 4, 1)
+    with pytest.raises(ValueError):
+        hb.from_arrays(np.array([0], np.uint32), np.array([5], np.uint32), 3)
+
+
+def test_validator_faults(cuda):
+    # test_acceptance.py:150-203 fault injection -> rules 2, 3, 5 (+1, 4, 6, 7)
+    hb = cuda
+    g = hb.generate_graph(hb.GraphParams(scale=8, edgefactor=8, seed=11))
+    r = hb.bfs(g, 0, device=False)
+    assert hb.validate_tree(g, 0, r.parent, r.level, check_minid=True).ok
+    par = r.parent.copy()
+    v = int(np.flatnonzero(par != hb.NIL)[1])
+    nbrs = set(int(x) for x in g.row(v))
+    par[v] = next(p for p in range(g.num_vertices) if p not in nbrs and p != v)
+    rep = hb.validate_tree(g, 0, par)
+    assert not rep.ok and rep.rule == 2 and rep.witness == v
+    bad = r.parent.copy()
+    bad[0] = 1
+    assert hb.validate_tree(g, 0, bad).rule == 1
+    gp, _, _ = graph(hb, [(0, 1), (1, 2), (2, 3)], 4)
+    tp = hb.bfs(gp, 0, device=False).parent.copy()
+    tp[2], tp[3] = 3, 2
+    assert hb.validate_tree(gp, 0, tp).rule == 3
+    gd, _, _ = graph(hb, [(0, 1), (2, 3)], 4)
+    td = hb.bfs(gd, 0, device=False).parent.copy()
+    td[2], td[3] = 3, 2
+    rep = hb.validate_tree(gd, 0, td)
+    assert rep.rule == 5 and rep.witness == 2
+    # rule 4: a chord spanning two levels: square 0-1-2-3-0 plus tail, claim 3's parent is 2
+    gs, _, _ = graph(hb, [(0, 1), (1, 2), (2, 3), (3, 0)], 4)
+    ts = hb.bfs(gs, 0, device=False)
+    t4 = ts.parent.copy()
+    t4[3] = 2  # 3 now at level 3, but edge (3,0) spans 3 levels
+    assert hb.validate_tree(gs, 0, t4).rule == 4
+    # rule 6: valid tree but not the min-id parent (triangle + square)
+    g6, _, _ = graph(hb, [(0, 1), (0, 2), (1, 3), (2, 3)], 4)
+    t6 = hb.bfs(g6, 0, device=False)
+    assert t6.parent[3] == 1
+    p6 = t6.parent.copy()
+    p6[3] = 2
+    assert hb.validate_tree(g6, 0, p6).ok
+    assert hb.validate_tree(g6, 0, p6, check_minid=True).rule == 6
+    lev = t6.level.copy()
+    lev[3] = 5
+    assert hb.validate_tree(g6, 0, t6.parent, lev).rule == 7
+
+
+def test_reference_csr_import(cuda, oracle):
+    hb = cuda
+    u, v = oracle.generate(9, 8, 3)
+    host = oracle.csr_build(u, v, 512)
+    g = hb.from_csr(host.row_starts, host.adjacency, host.in_edges_total)
+    assert g.num_arcs == host.num_arcs and g.in_edges_total == len(u)
+    tree, trace = hb.hybrid_bfs(host, 7)  # any object with the reference CsrGraph fields
+    par, lev, rows = oracle.hybrid_bfs(host, 7)
+    assert np.array_equal(tree.parent, par) and len(trace) == len(rows)

@@ -1,0 +1,197 @@
+"""CUDA path vs the reference (golden fixtures) and the pinned CPU oracle.
+
+Integer/index work throughout, so every comparison is bit-exact: device
+generator, device CSR (keep-dup and dedup), sampled roots, levels, parents
+(min-id rule), and the whole trace except `elapsed`.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["k8", "k10", "u12", "k11e4"]
+MODES = {
+    "simd_default": dict(use_simd=True),
+    "scalar_default": dict(use_simd=False),
+    "simd_a14b24": dict(use_simd=True, p=dict(alpha=14, beta=24)),
+    "simd_edge": dict(use_simd=True, p=dict(counter_mode="edge")),
+    "simd_maxpos3": dict(use_simd=True, cfg=dict(max_pos=3)),
+    "force_td": dict(use_simd=False, force_direction="top-down"),
+    "force_bu": dict(use_simd=True, force_direction="bottom-up"),
+}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def trace_array(trace):
+    return np.array([[r.layer, 1 if r.direction == "bottom-up" else 0, r.v_f, r.e_f, r.e_u,
+                      r.f_value, r.g_value, r.fallback_count, r.gather_count] for r in trace],
+                    dtype=np.int64).reshape(-1, 9)
+
+
+def run_mode(hb, g, s, mode, device=False):
+    kw = MODES[mode]
+    p = hb.HeuristicParams(**kw.get("p", {}))
+    cfg = hb.VecConfig(**kw.get("cfg", {}))
+    return hb.bfs(g, s, p, cfg, use_simd=kw["use_simd"], force_direction=kw.get("force_direction"),
+                  device=device)
+
+
+def params_of(meta):
+    import paper_1704_02259_b200 as hb
+
+    p = dict(meta["params"])
+    if "probs" in p:
+        p["probs"] = tuple(p["probs"])
+    return hb.GraphParams(**p)
+
+
+@pytest.fixture(scope="module")
+def small_graphs(cuda, golden_hashes):
+    hb = cuda
+    out = {}
+    for meta in golden_hashes["small"]:
+        params = params_of(meta)
+        out[meta["name"]] = (params, hb.build(hb.generate(params)))
+    return out
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_device_generator_and_csr(cuda, small_golden, small_graphs, name):
+    hb = cuda
+    params, g = small_graphs[name]
+    e = hb.generate(params)
+    assert np.array_equal(e.u, small_golden[f"{name}/u"])
+    assert np.array_equal(e.v, small_golden[f"{name}/v"])
+    assert np.array_equal(g.row_starts, small_golden[f"{name}/rs"])
+    assert np.array_equal(g.adjacency, small_golden[f"{name}/adj"])
+    gd = hb.generate_graph(params, dedup=True)
+    assert np.array_equal(gd.row_starts, small_golden[f"{name}/dedup_rs"])
+    assert np.array_equal(gd.adjacency, small_golden[f"{name}/dedup_adj"])
+    assert np.array_equal(hb.sample_sources(g, 8, 1), small_golden[f"{name}/sources"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_traversals_match_reference(cuda, small_golden, small_graphs, name):
+    hb = cuda
+    _, g = small_graphs[name]
+    for s in small_golden[f"{name}/sources"]:
+        s = int(s)
+        lev_ref = small_golden[f"{name}/{s}/level"]
+        for mode in MODES:
+            r = run_mode(hb, g, s, mode)
+            assert np.array_equal(r.level, lev_ref), (name, s, mode)
+            assert np.array_equal(r.parent, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
+            assert np.array_equal(trace_array(r.trace), small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)
+        # the reference-signature entry point returns the same tree
+        tree, trace = hb.hybrid_bfs(g, s, use_simd=True)
+        assert np.array_equal(tree.parent, small_golden[f"{name}/{s}/simd_default/parent"])
+        assert all(row.kernel == "simd" for row in trace)
+
+
+def test_device_outputs_and_validator(cuda, small_golden, small_graphs):
+    hb = cuda
+    _, g = small_graphs["k10"]
+    for s in small_golden["k10/sources"][:4]:
+        s = int(s)
+        r = run_mode(hb, g, s, "simd_a14b24", device=True)
+        par = r.parent.cpu().numpy().view(np.uint32)
+        lev = r.level.cpu().numpy()
+        assert np.array_equal(par, small_golden[f"k10/{s}/simd_a14b24/parent"])
+        assert np.array_equal(lev, small_golden[f"k10/{s}/level"])
+        rep = hb.validate_tree(g, s, r.parent, r.level, check_minid=True)
+        assert rep.ok, rep
+
+
+@pytest.mark.parametrize("heur", ["beamer", "reference"])
+@pytest.mark.parametrize("parent_mode", ["minid", "any"])
+def test_beamer_and_any_parent_vs_oracle(cuda, oracle, small_graphs, heur, parent_mode):
+    hb = cuda
+    _, g = small_graphs["u12"]
+    host = oracle.HostCsr(g.num_vertices, np.asarray(g.row_starts), np.asarray(g.adjacency),
+                          g.in_edges_total)
+    for s in oracle.sample_sources(host, 6, 3):
+        s = int(s)
+        p = hb.HeuristicParams(alpha=14, beta=24, heuristic=heur, counter_mode="edge")
+        r = hb.bfs(g, s, p, use_simd=True, parent_mode=parent_mode, device=False)
+        par, lev, rows = oracle.hybrid_bfs(host, s, heuristic=heur, counter_mode="edge", alpha=14,
+                                           beta=24, use_simd=True)
+        assert np.array_equal(r.level, lev)
+        got = trace_array(r.trace)
+        want = np.array([[x["layer"], x["direction"], x["v_f"], x["e_f"], x["e_u"], x["f_value"],
+                          x["g_value"], x["fallback_count"], x["gather_count"]] for x in rows])
+        assert np.array_equal(got, want)
+        if parent_mode == "minid":
+            assert np.array_equal(r.parent, par)
+        else:
+            assert hb.validate_tree(g, s, r.parent, r.level).ok
+
+
+def test_c1_kron_s16_all_roots(cuda, golden_hashes):
+    hb = cuda
+    rec = golden_hashes["configs"]["C1_kron_s16"]
+    g = hb.generate_graph(hb.GraphParams(scale=16, edgefactor=16, seed=1))
+    assert sha(g.row_starts) == rec["rs_sha"] and sha(g.adjacency) == rec["adj_sha"]
+    gd = hb.generate_graph(hb.GraphParams(scale=16, edgefactor=16, seed=1), dedup=True)
+    assert gd.num_arcs == rec["dedup_arcs"]
+    assert sha(gd.row_starts) == rec["dedup_rs_sha"] and sha(gd.adjacency) == rec["dedup_adj_sha"]
+    srcs = hb.sample_sources(g, 64, 1)
+    assert [int(x) for x in srcs] == rec["sources"]
+    for s in srcs:
+        r = rec["roots"][str(int(s))]
+        for mode in ("simd_default", "scalar_default", "simd_a14b24"):
+            out = run_mode(hb, g, int(s), mode)
+            assert sha(out.level) == r["level_sha"]
+            assert sha(out.parent) == r[mode]["parent_sha"]
+            assert trace_array(out.trace).tolist() == r[mode]["trace"]
+        # F2: dedup changes neither levels nor parents
+        outd = run_mode(hb, gd, int(s), "simd_a14b24")
+        assert sha(outd.level) == r["level_sha"]
+        assert sha(outd.parent) == r["simd_a14b24"]["parent_sha"]
+
+
+def test_c2_kron_s20_all_roots(cuda, golden_hashes):
+    hb = cuda
+    rec = golden_hashes["configs"]["C2_kron_s20"]
+    params = hb.GraphParams(scale=20, edgefactor=16, seed=1)
+    g = hb.generate_graph(params)
+    assert sha(g.row_starts) == rec["rs_sha"] and sha(g.adjacency) == rec["adj_sha"]
+    gd = hb.generate_graph(params, dedup=True)
+    assert gd.num_arcs == rec["dedup_arcs"] and sha(gd.adjacency) == rec["dedup_adj_sha"]
+    srcs = hb.sample_sources(g, 64, 1)
+    assert [int(x) for x in srcs] == rec["sources"]
+    for s in srcs:
+        r = rec["roots"][str(int(s))]
+        for mode in ("simd_a14b24", "simd_default"):
+            out = run_mode(hb, g, int(s), mode)
+            assert sha(out.level) == r["level_sha"]
+            assert sha(out.parent) == r[mode]["parent_sha"]
+            assert trace_array(out.trace).tolist() == r[mode]["trace"]
+        pb = hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge")
+        ob = hb.bfs(g, int(s), pb, device=False)
+        assert sha(ob.level) == r["level_sha"]
+        assert sha(ob.parent) == r["simd_a14b24"]["parent_sha"]
+
+
+def test_c3_uniform_s22_roots(cuda, golden_hashes):
+    hb = cuda
+    rec = golden_hashes["configs"]["C3_uniform_s22"]
+    params = hb.GraphParams(scale=22, edgefactor=16, seed=1, probs=(0.25,) * 4)
+    g = hb.generate_graph(params)
+    assert sha(g.row_starts) == rec["rs_sha"] and sha(g.adjacency) == rec["adj_sha"]
+    gd = hb.generate_graph(params, dedup=True)
+    assert gd.num_arcs == rec["dedup_arcs"] and sha(gd.adjacency) == rec["dedup_adj_sha"]
+    srcs = hb.sample_sources(g, 64, 1)
+    assert [int(x) for x in srcs] == rec["sources"]
+    for s, r in rec["roots"].items():
+        out = run_mode(hb, g, int(s), "simd_default")
+        assert sha(out.level) == r["level_sha"]
+        assert sha(out.parent) == r["simd_default"]["parent_sha"]
+        assert trace_array(out.trace).tolist() == r["simd_default"]["trace"]
