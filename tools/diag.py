@@ -1,0 +1,36 @@
+"""Per-layer timing breakdown of traversals (device globaltimer per layer)."""
+import argparse, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1704_02259_b200 as hb
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--scale", type=int, default=20)
+ap.add_argument("--uniform", action="store_true")
+ap.add_argument("--roots", type=int, default=8)
+ap.add_argument("--heuristic", default="beamer")
+ap.add_argument("--quiet", action="store_true")
+a = ap.parse_args()
+probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
+t0 = time.time()
+g = hb.generate_graph(hb.GraphParams(scale=a.scale, edgefactor=16, seed=1, probs=probs))
+torch.cuda.synchronize()
+print(f"graph S{a.scale}: n={g.num_vertices} arcs={g.num_arcs} maxdeg={g.max_degree} wide={g.wide_offsets} build {time.time()-t0:.2f}s", flush=True)
+roots = hb.sample_sources(g, 64, 1)[: a.roots]
+p = hb.HeuristicParams(alpha=14, beta=24, heuristic=a.heuristic, counter_mode="edge")
+n = g.num_vertices
+par = torch.empty(n, dtype=torch.int32, device="cuda"); lev = torch.empty_like(par)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for s in roots[:2]:
+    hb.bfs(g, int(s), p, device=True, out=(par, lev))
+tot = []
+for s in roots:
+    flush.fill_(1); torch.cuda.synchronize()
+    r = hb.bfs(g, int(s), p, device=True, out=(par, lev))
+    tot.append(r.device_seconds)
+    if not a.quiet:
+        lay = " ".join(f"{'B' if x.direction=='bottom-up' else 'T'}{x.v_f}:{x.elapsed*1e6:.1f}us" for x in r.trace)
+        print(f"root {int(s)}: {r.device_seconds*1e6:.1f}us  sum(layers)={sum(x.elapsed for x in r.trace)*1e6:.1f}us  {lay}", flush=True)
+m = g.in_edges_total
+print(f"hmean GTEPS {len(tot)*m/sum(tot)/1e9:.2f}  mean us {np.mean(tot)*1e6:.1f}")
