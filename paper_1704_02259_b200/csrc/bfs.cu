@@ -8,25 +8,29 @@
 // and the per-layer counters (bfs_scalar.py:18-26).
 //
 // Layout in HBM (per graph, reused by every root):
-//   rs     OffT[n+1]   row starts (uint32 when arcs < 2^32, else uint64)
-//   adj    u32[arcs]   sorted rows (csr.py:61-64)
-//   posw   u32[W]      deg>0 bitmap (engine.py:29-57 `posw`)
+//   rs     OffT[n+1]    row starts (uint32 when arcs < 2^32, else uint64)
+//   adj    u32[arcs]    sorted rows (csr.py:61-64)
+//   posw   u32[W]       deg>0 bitmap (engine.py:29-57 `posw`)
 //   parent u32[n], level i32[n]
-//   bits   u32[4W]     vis | bm0 | bm1 | bm2  — LSB-first bitmaps (frontier.py:3-6)
-//   q      u32[2n]     frontier queues (double-buffered)
-//   qo     OffT[2(n+1)] exclusive degree prefix of the queue (arc offsets)
+//   bits   u32[5W]      vis | B0 | B1 | B2 | B3 — LSB-first bitmaps (frontier.py:3-6)
+//   q/qo/qr             frontier queue: vertex, exclusive degree prefix (arc
+//                        offset), row start — double-buffered
+//   cs     u32[2*NC]    chunk starts: queue index holding arc c*kTdChunk
 //
-// Invariants at the start of layer L (depth d = L):
-//   in  = bm[L%3] = vertices at depth d (bitmap always valid)
-//   visited-before-layer = vis | in          (vis may lag by the frontier)
-//   out = bm[(L+1)%3] is all-zero; spare = bm[(L+2)%3] is cleared during L
-//   q[L%2]/qo[L%2] valid iff kind == 0 (frontier produced by a top-down layer)
+// Invariants at the start of layer L (frontier = depth L):
+//   in  = B[L%4] = frontier bitmap; out = B[(L+1)%4] is all-zero;
+//   spare = B[(L+2)%4] is cleared during L (B[(L+3)%4] is the previous frontier)
+//   vis | in = every vertex discovered so far (vis may lag by the frontier)
+//   queue buffer L%2 valid iff the frontier was produced top-down (kind 0)
 // Parents follow the reference's rule: the minimum-id neighbour one
-// level up — TD by atomicMin over all claimers, BU by first hit in the sorted
-// row (scans in ascending position order).
+// level up.  Bottom-up layers get it directly (first hit in the sorted row);
+// top-down layers take the atomicMin over every arc into a vertex unvisited
+// before the layer (parent_mode MINID).  parent_mode ANY lets the first
+// claimer win (one visited-bitmap claim per vertex, Graph500-valid trees).
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -85,16 +89,23 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
 }
 
 template <typename OffT>
+struct Queue {
+    uint32_t *q;   // vertex ids
+    OffT *qo;      // exclusive degree prefix
+    OffT *qr;      // row starts
+    uint32_t *cs;  // chunk starts
+};
+
+template <typename OffT>
 struct Args {
     const OffT *rs;
     const uint32_t *adj;
     const uint32_t *posw;
-    int64_t n, nw, arcs;
+    int64_t n, nw, arcs, ncs;
     uint32_t *parent;
     int32_t *level;
-    uint32_t *bits;  // vis | bm0 | bm1 | bm2
-    uint32_t *q;
-    OffT *qo;
+    uint32_t *bits;  // vis | B0..B3
+    Queue<OffT> qb[2];
     Ctl *ctl;
     hbfs_layer_row *rows;
     int64_t rows_cap;
@@ -125,7 +136,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // Largest index j in [0, len) with a[j] <= x (a non-decreasing, a[0] <= x).
 template <typename OffT>
 __device__ __forceinline__ int64_t last_le(const OffT *a, int64_t len, uint64_t x) {
-    int64_t lo = 0, hi = len;  // invariant: a[lo] <= x, answer in [lo, hi)
+    int64_t lo = 0, hi = len;
     while (hi - lo > 1) {
         int64_t mid = (lo + hi) >> 1;
         if ((uint64_t)a[mid] <= x) lo = mid; else hi = mid;
@@ -133,34 +144,93 @@ __device__ __forceinline__ int64_t last_le(const OffT *a, int64_t len, uint64_t 
     return lo;
 }
 
-// Warp-aggregated append of (v, deg) into a queue with its arc-offset prefix:
-// one 64-bit atomic per warp reserves both the slots and the arc range, so
-// queue order and prefix order agree (count<<35 | degree sum).
-template <typename OffT>
-__device__ __forceinline__ void warp_enqueue(bool claim, uint32_t v, uint64_t deg,
-                                             unsigned long long *counter, uint32_t *NQ,
-                                             OffT *NQO) {
+__device__ __forceinline__ bool test_bit(const uint32_t *bm, uint32_t a) {
+    return (bm[a >> 5] >> (a & 31)) & 1u;
+}
+
+// Warp-aggregated append to a queue: every lane contributes up to I entries
+// (v, deg, row start).  One 64-bit atomic per warp reserves both the queue slots
+// and the arc range (count<<35 | degree sum), so queue order and arc-prefix
+// order agree.  The warp also records, for every top-down chunk boundary
+// c*kTdChunk inside its arc range, the queue slot that holds it — the top-down
+// phase then needs no search to start a chunk.
+template <typename OffT, int I>
+__device__ __forceinline__ void warp_enqueue(const bool (&claim)[I], const uint32_t (&v)[I],
+                                             const uint64_t (&deg)[I], const OffT (&rsv)[I],
+                                             unsigned long long *counter, const Queue<OffT> &Q) {
     const unsigned full = 0xffffffffu;
-    const unsigned m = __ballot_sync(full, claim);
+    uint32_t cl = 0;
+    uint64_t dl = 0;
+#pragma unroll
+    for (int k = 0; k < I; ++k) {
+        cl += claim[k] ? 1u : 0u;
+        dl += claim[k] ? deg[k] : 0ull;
+    }
+    const unsigned m = __ballot_sync(full, cl != 0);
     if (!m) return;
     const int lane = threadIdx.x & 31;
-    uint64_t x = claim ? deg : 0;
+    uint32_t ci = cl;
+    uint64_t di = dl;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint64_t y = __shfl_up_sync(full, x, o);
-        if (lane >= o) x += y;
+        const uint32_t yc = __shfl_up_sync(full, ci, o);
+        const uint64_t yd = __shfl_up_sync(full, di, o);
+        if (lane >= o) {
+            ci += yc;
+            di += yd;
+        }
     }
-    const uint64_t total = __shfl_sync(full, x, 31);
-    const uint64_t excl = x - (claim ? deg : 0);
+    const uint64_t totc = __shfl_sync(full, ci, 31);
+    const uint64_t totd = __shfl_sync(full, di, 31);
     const int leader = __ffs(m) - 1;
     unsigned long long base = 0;
-    if (lane == leader)
-        base = atomicAdd(counter, ((unsigned long long)__popc(m) << kPackShift) + total);
+    if (lane == leader) base = atomicAdd(counter, (totc << kPackShift) + totd);
     base = __shfl_sync(full, base, leader);
-    if (claim) {
-        const uint64_t pos = (base >> kPackShift) + __popc(m & ((1u << lane) - 1));
-        NQ[pos] = v;
-        NQO[pos] = (OffT)((base & kPackMask) + excl);
+    const uint64_t qb = base >> kPackShift, db = base & kPackMask;
+    {
+        uint64_t pos = qb + ci - cl, off = db + di - dl;
+#pragma unroll
+        for (int k = 0; k < I; ++k) {
+            if (claim[k]) {
+                Q.q[pos] = v[k];
+                Q.qo[pos] = (OffT)off;
+                Q.qr[pos] = rsv[k];
+                ++pos;
+                off += deg[k];
+            }
+        }
+    }
+    if (totd == 0) return;
+    const uint64_t c_lo = (db + kTdChunk - 1) / kTdChunk;
+    const uint64_t c_hi = (db + totd - 1) / kTdChunk;
+    for (uint64_t c0 = c_lo; c0 <= c_hi; c0 += 32) {
+        const uint64_t c = c0 + lane;
+        const uint64_t t = c * kTdChunk - db;  // arc offset inside the warp's range
+        int l = 0;                              // lane whose range holds t
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint64_t val = __shfl_sync(full, di, l + step - 1);
+            if (val <= t) l += step;
+        }
+        if (l > 31) l = 31;
+        const uint64_t rel = t - (__shfl_sync(full, di, l) - __shfl_sync(full, dl, l));
+        uint32_t idx = 0;
+        uint64_t acc = 0;
+        bool found = false;
+#pragma unroll
+        for (int k = 0; k < I; ++k) {
+            const uint64_t dk = __shfl_sync(full, claim[k] ? deg[k] : 0ull, l);
+            const bool ck = __shfl_sync(full, claim[k] ? 1 : 0, l) != 0;
+            if (!found && ck) {
+                if (rel < acc + dk) found = true;
+                else {
+                    acc += dk;
+                    ++idx;
+                }
+            }
+        }
+        const uint64_t qpos = qb + (__shfl_sync(full, ci, l) - __shfl_sync(full, cl, l)) + idx;
+        if (c <= c_hi) Q.cs[c] = (uint32_t)qpos;
     }
 }
 
@@ -168,6 +238,111 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
     return x;
+}
+
+// First hit search.  Lane-parallel: for each k, an active lane searches its own
+// sorted row [s, e) for the first entry whose bit is set in `bm`, with aligned
+// uint4 loads (all K rows' loads in flight together).  Lanes unresolved after
+// kLaneVecs vectors are finished by a warp-cooperative scan, 128 entries per
+// step, lowest position winning (ballot + ffs) — the reference's first-hit rule
+// (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
+template <typename OffT, int K>
+__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const uint32_t *bm,
+                                           const bool (&act)[K], const OffT (&s)[K],
+                                           const OffT (&e)[K], int64_t (&hit)[K],
+                                           uint32_t (&hu)[K]) {
+    const int lane = threadIdx.x & 31;
+    OffT p[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        p[k] = s[k];
+        hit[k] = -1;
+        hu[k] = 0;
+    }
+#pragma unroll
+    for (int it = 0; it < kLaneVecs; ++it) {
+        uint4 q4[K];
+        bool go[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            go[k] = act[k] && hit[k] < 0 && p[k] < e[k];
+            if (go[k]) q4[k] = __ldg(reinterpret_cast<const uint4 *>(adj + (p[k] & ~(OffT)3)));
+            else q4[k] = make_uint4(0, 0, 0, 0);
+        }
+        uint32_t wd[K][4];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const OffT base = p[k] & ~(OffT)3;
+            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const OffT idx = base + j;
+                const bool ok = go[k] && idx >= p[k] && idx < e[k];
+                wd[k][j] = ok ? bm[val[j] >> 5] : 0u;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!go[k]) continue;
+            const OffT base = p[k] & ~(OffT)3;
+            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
+            uint32_t hm = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) hm |= ((wd[k][j] >> (val[j] & 31)) & 1u) << j;
+            // wd is 0 for out-of-row entries, so a set bit is always in range
+            if (hm) {
+                const int j = __ffs(hm) - 1;
+                hit[k] = (int64_t)(base + j);
+                hu[k] = val[j];
+            } else {
+                p[k] = base + 4;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        unsigned todo = __ballot_sync(0xffffffffu, act[k] && hit[k] < 0 && p[k] < e[k]);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint64_t ps = __shfl_sync(0xffffffffu, (unsigned long long)p[k], src);
+            const uint64_t pe = __shfl_sync(0xffffffffu, (unsigned long long)e[k], src);
+            int64_t h = -1;
+            uint32_t hv = 0;
+            for (uint64_t c = ps & ~3ull; c < pe; c += 128) {
+                const uint64_t b4 = c + 4 * lane;
+                uint32_t hm = 0;
+                uint4 q4 = make_uint4(0, 0, 0, 0);
+                if (b4 < pe) {
+                    q4 = __ldg(reinterpret_cast<const uint4 *>(adj + b4));
+                    const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t idx = b4 + j;
+                        if (idx >= ps && idx < pe && test_bit(bm, val[j])) hm |= 1u << j;
+                    }
+                }
+                const unsigned lanes = __ballot_sync(0xffffffffu, hm != 0);
+                if (lanes) {
+                    const int l = __ffs(lanes) - 1;
+                    const uint32_t hml = __shfl_sync(0xffffffffu, hm, l);
+                    const int j = __ffs(hml) - 1;
+                    const uint32_t vals[4] = {q4.x, q4.y, q4.z, q4.w};
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (jj == j) mine = vals[jj];
+                    hv = __shfl_sync(0xffffffffu, mine, l);
+                    h = (int64_t)(c + 4 * l + j);
+                    break;
+                }
+            }
+            if (lane == src) {
+                hit[k] = h;
+                hu[k] = hv;
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------- phases
@@ -182,12 +357,19 @@ __device__ void phase_init(const Args<OffT> &A) {
         A.parent[i] = r ? root : HBFS_NIL;
         A.level[i] = r ? 0 : -1;
     }
-    const int64_t rootw = A.nw + (root >> 5);  // bm0 word holding the root
-    for (int64_t w = tid; w < 4 * A.nw; w += nth)
-        A.bits[w] = (w == rootw) ? (1u << (root & 31)) : 0u;
+    // vis and B0 hold the root; B1..B3 zero
+    const int64_t rw = root >> 5;
+    const uint32_t rb = 1u << (root & 31);
+    for (int64_t w = tid; w < 5 * A.nw; w += nth)
+        A.bits[w] = (w == rw || w == A.nw + rw) ? rb : 0u;
+    const OffT r0 = __ldg(A.rs + root);
+    const uint64_t rdeg = (uint64_t)(__ldg(A.rs + root + 1) - r0);
+    const uint64_t nch = (rdeg + kTdChunk - 1) / kTdChunk;
+    for (int64_t c = tid; c < (int64_t)nch; c += nth) A.qb[0].cs[c] = 0;
     if (tid == 0) {
-        A.q[0] = root;
-        A.qo[0] = 0;
+        A.qb[0].q[0] = root;
+        A.qb[0].qo[0] = 0;
+        A.qb[0].qr[0] = r0;
         Ctl *c = A.ctl;
         for (int s = 0; s < 3; ++s) c->ctr[s] = Ctr{0, 0, 0, 0};
         c->conv = 0;
@@ -196,106 +378,151 @@ __device__ void phase_init(const Args<OffT> &A) {
 }
 
 // Top-down layer: arc-balanced expansion of the frontier queue.  CTA work item =
-// kTdChunk consecutive arcs of the concatenated frontier rows (so hubs of any
-// degree spread over many CTAs and adjacency reads are coalesced); each thread
-// maps its arc to (u, position) by binary search in the CTA's slice of the
-// degree prefix.  Replaces top_down_layer/top_down_chunked (_native.pyx:65-86,
+// kTdChunk consecutive arcs of the concatenated frontier rows, so hubs of any
+// degree spread over many CTAs and adjacency reads are coalesced; each thread
+// maps its kTdItems arcs to (u, position) by binary search in the CTA's
+// shared-memory slice of the degree prefix.  The items are staged (all
+// adjacency loads, then all visited-bit loads, then all claims) so their memory
+// latencies overlap.  A claim is one atomicOr on the L2-resident visited bitmap;
+// the claimer stamps the level and the warp enqueues all its claims with one
+// atomic.  Replaces top_down_layer / top_down_chunked (_native.pyx:65-86,
 // :207-239).
 template <typename OffT>
 __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, uint32_t *out,
                          uint32_t *spare, Ctr *ctr, TdSmem<OffT> &sm) {
+    constexpr int I = kTdItems;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int64_t cur = S.layer & 1;
-    const uint32_t *Q = A.q + cur * A.n;
-    const OffT *QO = A.qo + cur * (A.n + 1);
-    uint32_t *NQ = A.q + (1 - cur) * A.n;
-    OffT *NQO = A.qo + (1 - cur) * (A.n + 1);
+    const Queue<OffT> &Q = A.qb[S.layer & 1];
+    const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
     uint32_t *vis = A.bits;
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
     const int32_t depth1 = (int32_t)S.layer + 1;
+    const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
 
-    for (int64_t i = tid; i < nf; i += nth) {  // commit the frontier to vis
-        const uint32_t u = Q[i];
-        atomicOr(&vis[u >> 5], 1u << (u & 31));
-    }
     for (int64_t w = tid; w < A.nw; w += nth) spare[w] = 0;
+    if (!any_parent) {
+        // min-id mode keeps vis = "visited before the layer"; commit the
+        // frontier now (the tests below use vis | in, so no barrier is needed)
+        for (int64_t i = tid; i < nf; i += nth) {
+            const uint32_t x = Q.q[i];
+            atomicOr(&vis[x >> 5], 1u << (x & 31));
+        }
+    }
 
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const uint64_t a0 = (uint64_t)c * kTdChunk;
         const uint64_t a1 = min(a0 + (uint64_t)kTdChunk, mf);
         if (threadIdx.x == 0) {
-            const int64_t q0 = last_le(QO, nf, a0);
-            const int64_t q1 = last_le(QO, nf, a1 - 1);
+            const int64_t q0 = Q.cs[c];
+            const int64_t ql = (c + 1 < nchunks) ? (int64_t)Q.cs[c + 1] : nf - 1;
             sm.q0 = q0;
-            sm.cnt = q1 - q0 + 1;
+            sm.cnt = ql - q0 + 1;
         }
         __syncthreads();
         const int64_t q0 = sm.q0, cnt = sm.cnt;
         const bool in_smem = cnt <= kTdChunk + 2;
         if (in_smem) {
             for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-                const uint32_t u = Q[q0 + j];
-                sm.u[j] = u;
-                sm.off[j] = QO[q0 + j];
-                sm.rs[j] = __ldg(A.rs + u);
+                sm.u[j] = Q.q[q0 + j];
+                sm.off[j] = Q.qo[q0 + j];
+                sm.rs[j] = Q.qr[q0 + j];
             }
         }
         __syncthreads();
+        bool ok[I], claim[I];
+        uint32_t v[I], u[I], vw[I];
+        uint64_t deg[I];
+        OffT rsv[I];
 #pragma unroll
-        for (int k = 0; k < kTdItems; ++k) {
+        for (int k = 0; k < I; ++k) {
             const uint64_t a = a0 + (uint64_t)k * blockDim.x + threadIdx.x;
-            bool claim = false;
-            uint32_t v = 0;
-            uint64_t deg = 0;
-            if (a < a1) {
-                uint32_t u;
+            ok[k] = a < a1;
+            v[k] = u[k] = 0;
+            if (ok[k]) {
                 OffT off, rsu;
                 if (in_smem) {
                     const int64_t j = last_le(sm.off, cnt, a);
                     off = sm.off[j];
-                    u = sm.u[j];
+                    u[k] = sm.u[j];
                     rsu = sm.rs[j];
                 } else {
-                    const int64_t j = q0 + last_le(QO + q0, nf - q0, a);
-                    off = QO[j];
-                    u = Q[j];
-                    rsu = __ldg(A.rs + u);
+                    const int64_t j = q0 + last_le(Q.qo + q0, nf - q0, a);
+                    off = Q.qo[j];
+                    u[k] = Q.q[j];
+                    rsu = Q.qr[j];
                 }
-                v = __ldg(A.adj + (uint64_t)rsu + (a - (uint64_t)off));
-                const uint32_t w = v >> 5, b = 1u << (v & 31);
-                const uint32_t seen = vis[w] | in[w];
-                if (!(seen & b)) {
-                    uint32_t old = out[w];
-                    if (!(old & b)) old = atomicOr(&out[w], b);
-                    claim = !(old & b);
-                    if (A.parent_mode == HBFS_PARENT_MINID) atomicMin(&A.parent[v], u);
-                    else if (claim) A.parent[v] = u;
-                    if (claim) {
-                        A.level[v] = depth1;
-                        deg = (uint64_t)(__ldg(A.rs + v + 1) - __ldg(A.rs + v));
-                    }
+                v[k] = __ldg(A.adj + (uint64_t)rsu + (a - (uint64_t)off));
+            }
+        }
+        if (any_parent) {
+            // claim on the visited bitmap itself: one L2 load per arc
+#pragma unroll
+            for (int k = 0; k < I; ++k) vw[k] = ok[k] ? vis[v[k] >> 5] : ~0u;
+#pragma unroll
+            for (int k = 0; k < I; ++k) {
+                const uint32_t b = 1u << (v[k] & 31);
+                claim[k] = false;
+                if (!(vw[k] & b)) claim[k] = !(atomicOr(&vis[v[k] >> 5], b) & b);
+            }
+        } else {
+            // min-id parents: every arc into a vertex unvisited before the layer
+            // takes part in an atomicMin, so `visited` must mean "before this
+            // layer" (vis | in); claims go to `out`.
+            uint32_t ow[I];
+#pragma unroll
+            for (int k = 0; k < I; ++k) {
+                vw[k] = ok[k] ? (vis[v[k] >> 5] | in[v[k] >> 5]) : ~0u;
+                ow[k] = ok[k] ? out[v[k] >> 5] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < I; ++k) {
+                const uint32_t b = 1u << (v[k] & 31);
+                claim[k] = false;
+                if (!(vw[k] & b)) {
+                    uint32_t old = ow[k];
+                    if (!(old & b)) old = atomicOr(&out[v[k] >> 5], b);
+                    claim[k] = !(old & b);
+                    atomicMin(&A.parent[v[k]], u[k]);
                 }
             }
-            warp_enqueue(claim, v, deg, &ctr->packed, NQ, NQO);
         }
+#pragma unroll
+        for (int k = 0; k < I; ++k) {
+            deg[k] = 0;
+            rsv[k] = 0;
+            if (claim[k]) {
+                if (any_parent) {
+                    atomicOr(&out[v[k] >> 5], 1u << (v[k] & 31));
+                    A.parent[v[k]] = u[k];
+                }
+                A.level[v[k]] = depth1;
+                rsv[k] = __ldg(A.rs + v[k]);
+                deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - rsv[k]);
+            }
+        }
+        warp_enqueue<OffT, I>(claim, v, deg, rsv, &ctr->packed, NQ);
         __syncthreads();
     }
 }
 
-// Bottom-up layer: one warp per 32-vertex bitmap word (the warp owns the word,
-// so vis/out updates are plain stores).  Each lane probes its own sorted row in
-// ascending position with aligned uint4 loads; lanes still unresolved after
-// kLaneVecs vectors hand their remaining row to a warp-cooperative scan that
-// takes the lowest hit position (ballot + ffs), preserving the reference's
-// first-hit rule.  Counters gathers/fallbacks are those the reference's
-// 16-lane kernel would report.  Replaces bottom_up_multiple_set /
-// bottom_up_layer (_native.pyx:89-204, bu_probe.h:22-106).
-template <typename OffT>
+// Bottom-up layer.  A warp takes a tile of 32 bitmap words (one per lane), so
+// finished words are skipped 32 at a time.  The tile's candidates (unvisited,
+// degree > 0) are compacted across the lanes — every lane works regardless of
+// how candidates are spread over words — and each lane runs C independent
+// first-hit searches at once (first_hits: uint4 row probes against the
+// frontier bitmap, warp-cooperative scan for long rows).  Found bits gather in
+// the warp's shared-memory copy of the tile, then one plain store per word
+// updates out/vis (the warp owns its words).  Counters gathers/fallbacks are
+// those of the reference's 16-lane kernel.  Replaces
+// bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
+// bu_probe.h:22-106).
+template <typename OffT, int C>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const uint32_t *in, uint32_t *out,
-                         uint32_t *spare, Ctr *ctr, unsigned long long *red) {
+                         uint32_t *spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
+    const unsigned full = 0xffffffffu;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
@@ -303,138 +530,114 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const uint32_t *in, u
     uint32_t *vis = A.bits;
     const int32_t depth1 = (int32_t)S.layer + 1;
     const int64_t max_pos = A.max_pos;
-    unsigned long long c_cnt = 0, c_deg = 0, c_gat = 0, c_fb = 0;
+    // packed per-thread counters: found<<35 | their degree sum ; fallbacks<<35 | gathers
+    unsigned long long c_fd = 0, c_fg = 0;
+    const int64_t ntiles = (A.nw + 31) >> 5;
 
-    for (int64_t w = tid; w < A.nw; w += nth) spare[w] = 0;
-
-    for (int64_t w = gwarp; w < A.nw; w += nwarps) {
-        const uint32_t vw = vis[w], iw = in[w], pw = __ldg(A.posw + w);
-        const uint32_t visited = vw | iw;
-        const uint32_t cand = ~visited & pw;
-        if (!cand) {
-            if (lane == 0 && iw && (vw | iw) != vw) vis[w] = visited;
-            continue;
-        }
-        const bool mine = (cand >> lane) & 1u;
-        const uint64_t v = (uint64_t)w * 32 + lane;
-        OffT s = 0, e = 0;
-        if (mine) {
-            s = __ldg(A.rs + v);
-            e = __ldg(A.rs + v + 1);
-        }
-        int64_t hit = -1;  // absolute adjacency index of the first frontier neighbour
-        uint32_t hit_u = 0;
-        OffT p = s;
-        if (mine) {
+    for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+        const int64_t wl = tile * 32 + lane;
+        const bool valid = wl < A.nw;
+        const uint32_t vis0 = valid ? vis[wl] : ~0u;
+        const uint32_t inl = valid ? in[wl] : 0u;
+        const uint32_t pwl = valid ? __ldg(A.posw + wl) : 0u;
+        if (valid) spare[wl] = 0;
+        const uint32_t vwl = vis0 | inl;
+        const uint32_t candl = ~vwl & pwl;
+        if (valid && vwl != vis0) vis[wl] = vwl;  // commit a lagging frontier
+        const uint32_t cntl = __popc(candl);
+        uint32_t incl = cntl;
 #pragma unroll
-            for (int it = 0; it < kLaneVecs; ++it) {
-                if (p >= e) break;
-                const OffT base = p & ~(OffT)3;
-                const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(A.adj + base));
-                const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
-                uint32_t hm = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(full, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t T = __shfl_sync(full, incl, 31);
+        if (T == 0) continue;
+        s_found[lane] = 0;
+        __syncwarp();
+        for (uint32_t b = 0; b < T; b += 32 * C) {
+            bool act[C];
+            OffT s[C], e[C];
+            uint32_t v[C];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const OffT idx = base + j;
-                    if (idx >= p && idx < e) {
-                        const uint32_t a = val[j];
-                        if ((in[a >> 5] >> (a & 31)) & 1u) hm |= 1u << j;
-                    }
+            for (int k = 0; k < C; ++k) {
+                const uint32_t c = b + k * 32 + lane;
+                act[k] = c < T;
+                int j = 0;  // word holding candidate c: lanes with incl <= c
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const uint32_t val = __shfl_sync(full, incl, j + step - 1);
+                    if (val <= c) j += step;
                 }
-                if (hm) {
-                    const int j = __ffs(hm) - 1;
-                    hit = (int64_t)(base + j);
-                    hit_u = val[j];
-                    break;
-                }
-                p = base + 4;
-            }
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, mine && hit < 0 && p < e);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint64_t ps = (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)p, src);
-            const uint64_t pe = (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
-            int64_t h = -1;
-            uint32_t hu = 0;
-            for (uint64_t c = ps; c < pe; c += 32) {
-                const uint64_t idx = c + lane;
-                bool bit = false;
-                uint32_t a = 0;
-                if (idx < pe) {
-                    a = __ldg(A.adj + idx);
-                    bit = (in[a >> 5] >> (a & 31)) & 1u;
-                }
-                const unsigned hb = __ballot_sync(0xffffffffu, bit);
-                if (hb) {
-                    const int l = __ffs(hb) - 1;
-                    h = (int64_t)(c + l);
-                    hu = __shfl_sync(0xffffffffu, a, l);
-                    break;
+                if (j > 31) j = 31;
+                const uint32_t cm = __shfl_sync(full, candl, j);
+                const uint32_t ex = __shfl_sync(full, incl, j) - __shfl_sync(full, cntl, j);
+                const uint32_t bit = act[k] ? __fns(cm, 0, (int)(c - ex) + 1) : 0u;
+                v[k] = (uint32_t)((tile * 32 + j) * 32 + bit);
+                s[k] = e[k] = 0;
+                if (act[k]) {
+                    s[k] = __ldg(A.rs + v[k]);
+                    e[k] = __ldg(A.rs + v[k] + 1);
                 }
             }
-            if (lane == src && h >= 0) {
-                hit = h;
-                hit_u = hu;
+            int64_t hit[C];
+            uint32_t hu[C];
+            first_hits<OffT, C>(A.adj, in, act, s, e, hit, hu);
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                if (!act[k]) continue;
+                const bool found = hit[k] >= 0;
+                const int64_t deg = (int64_t)(e[k] - s[k]);
+                const int64_t pos = found ? hit[k] - (int64_t)s[k] : -1;
+                const bool early = found && pos < max_pos;
+                if (found) {
+                    A.parent[v[k]] = hu[k];
+                    A.level[v[k]] = depth1;
+                    atomicOr(&s_found[(v[k] >> 5) - tile * 32], 1u << (v[k] & 31));
+                    c_fd += (1ull << kPackShift) + (unsigned long long)deg;
+                }
+                c_fg += (unsigned long long)(early ? pos + 1 : (deg < max_pos ? deg : max_pos));
+                if (deg > max_pos && !early) c_fg += 1ull << kPackShift;
             }
         }
-        const bool found = hit >= 0;
-        if (found) {
-            A.parent[v] = hit_u;
-            A.level[v] = depth1;
+        __syncwarp();
+        const uint32_t f = s_found[lane];
+        if (valid && f) {
+            out[wl] = f;
+            vis[wl] = vwl | f;
         }
-        const unsigned fm = __ballot_sync(0xffffffffu, found);
-        if (lane == 0) {
-            if (fm) out[w] = fm;
-            if ((iw | fm) && (visited | fm) != vw) vis[w] = visited | fm;
-        }
-        if (mine) {
-            const int64_t deg = (int64_t)(e - s);
-            const int64_t pos = found ? hit - (int64_t)s : -1;
-            const bool early = found && pos < max_pos;
-            if (found) {
-                c_cnt += 1;
-                c_deg += (unsigned long long)deg;
-            }
-            c_gat += early ? (unsigned long long)(pos + 1)
-                           : (unsigned long long)(deg < max_pos ? deg : max_pos);
-            c_fb += (deg > max_pos && !early) ? 1ull : 0ull;
-        }
+        __syncwarp();
     }
     // CTA reduction of the counters, one atomic per CTA per counter.
-    c_cnt = warp_sum(c_cnt);
-    c_deg = warp_sum(c_deg);
-    c_gat = warp_sum(c_gat);
-    c_fb = warp_sum(c_fb);
+    c_fd = warp_sum(c_fd);
+    c_fg = warp_sum(c_fg);
     const int wid = threadIdx.x >> 5;
     if (lane == 0) {
-        red[wid * 4 + 0] = c_cnt;
-        red[wid * 4 + 1] = c_deg;
-        red[wid * 4 + 2] = c_gat;
-        red[wid * 4 + 3] = c_fb;
+        red[wid * 2 + 0] = c_fd;
+        red[wid * 2 + 1] = c_fg;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long t[4] = {0, 0, 0, 0};
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
-            for (int k = 0; k < 4; ++k) t[k] += red[i * 4 + k];
-        if (t[0] | t[1]) atomicAdd(&ctr->packed, (t[0] << kPackShift) + t[1]);
-        if (t[2]) atomicAdd(&ctr->gathers, t[2]);
-        if (t[3]) atomicAdd(&ctr->fallbacks, t[3]);
+        unsigned long long t0 = 0, t1 = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            t0 += red[i * 2 + 0];
+            t1 += red[i * 2 + 1];
+        }
+        if (t0) atomicAdd(&ctr->packed, t0);
+        if (t1 & kPackMask) atomicAdd(&ctr->gathers, t1 & kPackMask);
+        if (t1 >> kPackShift) atomicAdd(&ctr->fallbacks, t1 >> kPackShift);
     }
     __syncthreads();
 }
 
-// Bitmap -> queue (with arc-offset prefix) at a bottom-up -> top-down switch.
+// Bitmap -> queue (with arc prefix, row starts, chunk starts) at a bottom-up ->
+// top-down switch.
 template <typename OffT>
 __device__ void phase_convert(const Args<OffT> &A, const St &S, const uint32_t *in) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    const int64_t cur = S.layer & 1;
-    uint32_t *Q = A.q + cur * A.n;
-    OffT *QO = A.qo + cur * (A.n + 1);
+    const Queue<OffT> &Q = A.qb[S.layer & 1];
     for (int64_t w0 = tid - lane; w0 < A.nw; w0 += nth) {
         const int64_t w = w0 + lane;
         uint32_t bits = w < A.nw ? in[w] : 0u;
@@ -442,21 +645,30 @@ __device__ void phase_convert(const Args<OffT> &A, const St &S, const uint32_t *
             const bool has = bits != 0;
             uint32_t v = 0;
             uint64_t deg = 0;
+            OffT r0 = 0;
             if (has) {
                 v = (uint32_t)(w * 32 + __ffs(bits) - 1);
                 bits &= bits - 1;
-                deg = (uint64_t)(__ldg(A.rs + v + 1) - __ldg(A.rs + v));
+                r0 = __ldg(A.rs + v);
+                deg = (uint64_t)(__ldg(A.rs + v + 1) - r0);
             }
-            warp_enqueue(has, v, deg, &A.ctl->conv, Q, QO);
+            const bool hk[1] = {has};
+            const uint32_t vk[1] = {v};
+            const uint64_t dk[1] = {deg};
+            const OffT rk[1] = {r0};
+            warp_enqueue<OffT, 1>(hk, vk, dk, rk, &A.ctl->conv, Q);
         }
     }
 }
 
-template <typename OffT>
-__global__ void __launch_bounds__(kBlock) bfs_kernel(Args<OffT> A) {
+// K: first-hit searches in flight per lane in the bottom-up phase;
+// MINB: CTAs per SM the register allocation must allow.
+template <typename OffT, int K, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     cg::grid_group grid = cg::this_grid();
     __shared__ TdSmem<OffT> sm;
     __shared__ unsigned long long red[(kBlock / 32) * 4];
+    __shared__ uint32_t s_found[kBlock];  // per warp: found bits of its 32-word tile
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
 
     St S;
@@ -490,9 +702,10 @@ __global__ void __launch_bounds__(kBlock) bfs_kernel(Args<OffT> A) {
         int64_t fv, gv;
         const int dir = decide(A.H, S.dir, S.v_f, S.e_f, S.eu_v, S.eu_e, S.prev_vf, &fv, &gv);
         const int64_t L = S.layer;
-        const uint32_t *in = A.bits + A.nw * (1 + L % 3);
-        uint32_t *out = A.bits + A.nw * (1 + (L + 1) % 3);
-        uint32_t *spare = A.bits + A.nw * (1 + (L + 2) % 3);
+        uint32_t *B = A.bits + A.nw;
+        const uint32_t *in = B + A.nw * (L % 4);
+        uint32_t *out = B + A.nw * ((L + 1) % 4);
+        uint32_t *spare = B + A.nw * ((L + 2) % 4);
         Ctr *ctr = &A.ctl->ctr[L % 3];
         if (dir == HBFS_TOP_DOWN && S.kind == 1) {
             phase_convert(A, S, in);
@@ -506,7 +719,7 @@ __global__ void __launch_bounds__(kBlock) bfs_kernel(Args<OffT> A) {
             A.ctl->conv = 0;
         }
         if (dir == HBFS_TOP_DOWN) phase_td(A, S, in, out, spare, ctr, sm);
-        else phase_bu(A, S, in, out, spare, ctr, red);
+        else phase_bu<OffT, K>(A, S, in, out, spare, ctr, red, s_found + (threadIdx.x & ~31));
         grid.sync();
 
         const unsigned long long packed = __ldcg(&ctr->packed);
@@ -561,13 +774,44 @@ __global__ void __launch_bounds__(kBlock) bfs_kernel(Args<OffT> A) {
     }
 }
 
+// ------------------------------------------------------------ variants
+
+// Kernel variants compiled into the library (occupancy/MLP trade-offs);
+// HBFS_KERNEL_VARIANT=<index> selects one, default kDefaultVariant.
+template <typename OffT>
+struct Variant {
+    const void *fn;
+    int k, minb;
+};
+
+template <typename OffT>
+static const Variant<OffT> *variants(int *count) {
+    static const Variant<OffT> v[] = {
+        {(const void *)bfs_kernel<OffT, 2, 1>, 2, 1},
+        {(const void *)bfs_kernel<OffT, 1, 1>, 1, 1},
+        {(const void *)bfs_kernel<OffT, 1, 2>, 1, 2},
+        {(const void *)bfs_kernel<OffT, 2, 2>, 2, 2},
+        {(const void *)bfs_kernel<OffT, 4, 1>, 4, 1},
+    };
+    *count = (int)(sizeof(v) / sizeof(v[0]));
+    return v;
+}
+constexpr int kDefaultVariant = 0;
+
+static int variant_index() {
+    const char *e = getenv("HBFS_KERNEL_VARIANT");
+    return e ? atoi(e) : kDefaultVariant;
+}
+
 // ------------------------------------------------------------ workspace
 
 struct Workspace {
     int64_t n = 0;
     int wide = 0;
-    DevBuf parent, level, bits, q, qo, ctl;  // ctl: Ctl followed by kRowsCap rows
+    DevBuf parent, level, bits, q, qo, qr, cs, ctl;  // ctl: Ctl followed by kRowsCap rows
+    int64_t ncs = 0;  // chunk-start entries per queue buffer
     int grid = 0;
+    const void *fn = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     void *h_ctl = nullptr;  // pinned mirror of ctl + rows
     ~Workspace() {
@@ -587,9 +831,12 @@ static int ws_alloc(hbfs_graph *g) {
     int rc = HBFS_OK;
     if (!rc) rc = w->parent.alloc(n * 4);
     if (!rc) rc = w->level.alloc(n * 4);
-    if (!rc) rc = w->bits.alloc(4 * nw * 4 + 16);
-    if (!rc) rc = w->q.alloc(2 * n * 4 + 16);
+    w->ncs = g->arcs / kTdChunk + 2;
+    if (!rc) rc = w->bits.alloc(5 * nw * 4 + 16);
+    if (!rc) rc = w->q.alloc(2 * (n + 1) * 4 + 16);
     if (!rc) rc = w->qo.alloc(2 * (n + 1) * sizeof(OffT));
+    if (!rc) rc = w->qr.alloc(2 * (n + 1) * sizeof(OffT));
+    if (!rc) rc = w->cs.alloc(2 * w->ncs * 4);
     if (!rc) rc = w->ctl.alloc(ctl_bytes());
     if (!rc && cudaMallocHost(&w->h_ctl, ctl_bytes()) != cudaSuccess)
         rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
@@ -599,7 +846,12 @@ static int ws_alloc(hbfs_graph *g) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel<OffT>, kBlock, 0);
+        int nv = 0;
+        const Variant<OffT> *vt = variants<OffT>(&nv);
+        int vi = variant_index();
+        if (vi < 0 || vi >= nv) vi = kDefaultVariant;
+        w->fn = vt[vi].fn;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w->fn, kBlock, 0);
         if (e != cudaSuccess || per_sm < 1)
             rc = set_error(HBFS_ECUDA, "occupancy query failed: %s", cudaGetErrorString(e));
         w->grid = per_sm * sms;
@@ -631,8 +883,13 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.parent = (dev_out && parent) ? parent : w->parent.as<uint32_t>();
     A.level = (dev_out && level) ? level : w->level.as<int32_t>();
     A.bits = w->bits.as<uint32_t>();
-    A.q = w->q.as<uint32_t>();
-    A.qo = w->qo.as<OffT>();
+    A.ncs = w->ncs;
+    for (int b = 0; b < 2; ++b) {
+        A.qb[b].q = w->q.as<uint32_t>() + b * (g->n + 1);
+        A.qb[b].qo = w->qo.as<OffT>() + b * (g->n + 1);
+        A.qb[b].qr = w->qr.as<OffT>() + b * (g->n + 1);
+        A.qb[b].cs = w->cs.as<uint32_t>() + b * w->ncs;
+    }
     A.ctl = w->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(w->ctl.as<char>() + sizeof(Ctl));
     A.rows_cap = kRowsCap;
@@ -655,7 +912,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     for (int launch = 0;; ++launch) {
         A.do_init = launch == 0;
         void *kargs[] = {&A};
-        HB_CUDA(cudaLaunchCooperativeKernel((const void *)bfs_kernel<OffT>, dim3(w->grid),
+        HB_CUDA(cudaLaunchCooperativeKernel(w->fn, dim3(w->grid),
                                             dim3(kBlock), kargs, 0, st));
         HB_CUDA(cudaEventRecord(w->ev1, st));
         // Ctl plus the first rows in one copy; the rest only if needed.

@@ -11,6 +11,7 @@ ap.add_argument("--uniform", action="store_true")
 ap.add_argument("--roots", type=int, default=8)
 ap.add_argument("--heuristic", default="beamer")
 ap.add_argument("--quiet", action="store_true")
+ap.add_argument("--parent-mode", default="minid")
 a = ap.parse_args()
 probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
 t0 = time.time()
@@ -23,11 +24,11 @@ n = g.num_vertices
 par = torch.empty(n, dtype=torch.int32, device="cuda"); lev = torch.empty_like(par)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for s in roots[:2]:
-    hb.bfs(g, int(s), p, device=True, out=(par, lev))
+    hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
 tot = []
 for s in roots:
     flush.fill_(1); torch.cuda.synchronize()
-    r = hb.bfs(g, int(s), p, device=True, out=(par, lev))
+    r = hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
     tot.append(r.device_seconds)
     if not a.quiet:
         lay = " ".join(f"{'B' if x.direction=='bottom-up' else 'T'}{x.v_f}:{x.elapsed*1e6:.1f}us" for x in r.trace)
