@@ -798,9 +798,13 @@ static const Variant<OffT> *variants(int *count) {
 }
 constexpr int kDefaultVariant = 0;
 
-static int variant_index() {
+// Measured on B200 (tools/diag.py sweeps): small graphs are latency-bound and
+// prefer one fat CTA per SM with 4 searches in flight per lane (variant 4);
+// SCALE >= 24 prefers two CTAs per SM with 2 searches per lane (variant 3).
+static int variant_index(int64_t n) {
     const char *e = getenv("HBFS_KERNEL_VARIANT");
-    return e ? atoi(e) : kDefaultVariant;
+    if (e) return atoi(e);
+    return n >= (int64_t(1) << 24) ? 3 : 4;
 }
 
 // ------------------------------------------------------------ workspace
@@ -848,7 +852,7 @@ static int ws_alloc(hbfs_graph *g) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         int nv = 0;
         const Variant<OffT> *vt = variants<OffT>(&nv);
-        int vi = variant_index();
+        int vi = variant_index(n);
         if (vi < 0 || vi >= nv) vi = kDefaultVariant;
         w->fn = vt[vi].fn;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w->fn, kBlock, 0);

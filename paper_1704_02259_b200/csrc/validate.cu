@@ -129,16 +129,25 @@ __global__ void k_rule4(int64_t n, const OffT *rs, const uint32_t *adj, const in
 template <typename OffT>
 __global__ void k_rule6(int64_t n, int64_t root, const OffT *rs, const uint32_t *adj,
                         const int32_t *plev, const uint32_t *parent, unsigned long long *wit) {
-    GSTRIDE(v, n) {
+    // warp per vertex: the first neighbour one level up in the sorted row (min id)
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t p = parent[v];
         if (p == HBFS_NIL || v == root) continue;
         const int32_t want = plev[v] - 1;
         uint32_t best = HBFS_NIL;
-        for (uint64_t k = rs[v]; k < (uint64_t)rs[v + 1]; ++k) {
-            const uint32_t w = adj[k];
-            if (plev[w] == want) { best = w; break; }  // rows ascending: first = min id
+        for (uint64_t k0 = rs[v]; k0 < (uint64_t)rs[v + 1]; k0 += 32) {
+            const uint64_t k = k0 + lane;
+            uint32_t w = 0;
+            const bool hit = k < (uint64_t)rs[v + 1] && plev[(w = adj[k])] == want;
+            const unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (b) {
+                best = __shfl_sync(0xffffffffu, w, __ffs(b) - 1);
+                break;
+            }
         }
-        if (best != p) atomicMin(wit, (unsigned long long)v);
+        if (lane == 0 && best != p) atomicMin(wit, (unsigned long long)v);
     }
 }
 
@@ -248,7 +257,7 @@ static int validate_impl(hbfs_graph *g, int64_t root, const uint32_t *parent, co
     if (w >= 0) { *rule = 4; *witness = w; return HBFS_OK; }
     if (check_minid) {
         HB_CHECK(P.reset(st));
-        k_rule6<OffT><<<vgrid(n), 256, 0, st>>>(n, root, rs, adj, plev, parent, P.wit);
+        k_rule6<OffT><<<vgrid(n * 32), 256, 0, st>>>(n, root, rs, adj, plev, parent, P.wit);
         HB_CUDA(cudaGetLastError());
         HB_CHECK(P.read(st, &w));
         if (w >= 0) { *rule = 6; *witness = w; return HBFS_OK; }
@@ -298,29 +307,38 @@ __global__ void k_acc_td(int64_t n, int32_t d, const int32_t *level, const OffT 
 
 // BU layer: U = unvisited before the layer with deg > 0; probes(v) = 1 + first
 // position of a depth-d neighbour if v is found (level d+1), else deg(v).
+// Warp per vertex (rows can be millions of entries long).
 template <typename OffT>
 __global__ void k_acc_bu(int64_t n, int32_t d, const int32_t *level, const OffT *rs,
                          const uint32_t *adj, int rs_bytes, uint32_t *f_rs, uint32_t *f_adj,
                          uint32_t *f_bm, unsigned long long *cnt) {
-    GSTRIDE(v, n) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int32_t lv = level[v];
         if (!(lv == -1 || lv > d)) continue;
         const uint64_t s = rs[v], e = rs[v + 1];
-        atomicAdd(&cnt[0], 1ull);  // |U|
+        if (lane == 0) atomicAdd(&cnt[0], 1ull);  // |U|
         if (e == s) continue;
-        mark(f_rs, (uint64_t)v * rs_bytes / 32);
-        mark(f_rs, (uint64_t)(v + 1) * rs_bytes / 32);
+        if (lane == 0) {
+            mark(f_rs, (uint64_t)v * rs_bytes / 32);
+            mark(f_rs, (uint64_t)(v + 1) * rs_bytes / 32);
+        }
         uint64_t probes = e - s;
         if (lv == d + 1) {
-            for (uint64_t k = s; k < e; ++k) {
-                if (level[adj[k]] == d) { probes = k - s + 1; break; }
+            for (uint64_t k0 = s; k0 < e; k0 += 32) {
+                const uint64_t k = k0 + lane;
+                const bool hit = k < e && level[adj[k]] == d;
+                const unsigned b = __ballot_sync(0xffffffffu, hit);
+                if (b) {
+                    probes = k0 + (__ffs(b) - 1) - s + 1;
+                    break;
+                }
             }
         }
-        atomicAdd(&cnt[1], (unsigned long long)probes);
-        uint64_t last = ~0ull;
-        for (uint64_t k = s; k < s + probes; ++k) {
-            const uint64_t sec = k * 4 / 32;
-            if (sec != last) { mark(f_adj, sec); last = sec; }
+        if (lane == 0) atomicAdd(&cnt[1], (unsigned long long)probes);
+        for (uint64_t k = s + lane; k < s + probes; k += 32) {
+            mark(f_adj, k * 4 / 32);
             mark(f_bm, (uint64_t)(adj[k] >> 5) * 4 / 32);
         }
     }
@@ -379,7 +397,7 @@ static int bytes_impl(hbfs_graph *g, int64_t root, const int32_t *level,
             k_acc_td<OffT><<<vgrid(n * 32), 256, 0, st>>>(n, d, level, rs, adj, rs_bytes, f_rs.as<uint32_t>(),
                                                          f_adj.as<uint32_t>(), f_bm.as<uint32_t>(), c);
         else
-            k_acc_bu<OffT><<<vgrid(n), 256, 0, st>>>(n, d, level, rs, adj, rs_bytes, f_rs.as<uint32_t>(),
+            k_acc_bu<OffT><<<vgrid(n * 32), 256, 0, st>>>(n, d, level, rs, adj, rs_bytes, f_rs.as<uint32_t>(),
                                                     f_adj.as<uint32_t>(), f_bm.as<uint32_t>(), c);
         HB_CUDA(cudaGetLastError());
         k_acc_new<<<vgrid(n), 256, 0, st>>>(n, d, level, f_pl.as<uint32_t>(), c);

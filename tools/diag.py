@@ -31,7 +31,7 @@ for s in roots:
     r = hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
     tot.append(r.device_seconds)
     if not a.quiet:
-        lay = " ".join(f"{'B' if x.direction=='bottom-up' else 'T'}{x.v_f}:{x.elapsed*1e6:.1f}us" for x in r.trace)
+        lay = " ".join(f"{"B" if x.direction=="bottom-up" else "T"}{x.v_f}[{x.e_f/1e6:.1f}M]:{x.elapsed*1e6:.1f}us" for x in r.trace)
         print(f"root {int(s)}: {r.device_seconds*1e6:.1f}us  sum(layers)={sum(x.elapsed for x in r.trace)*1e6:.1f}us  {lay}", flush=True)
 m = g.in_edges_total
 print(f"hmean GTEPS {len(tot)*m/sum(tot)/1e9:.2f}  mean us {np.mean(tot)*1e6:.1f}")
