@@ -104,7 +104,7 @@ struct Args {
     int64_t n, nw, arcs, ncs;
     uint32_t *parent;
     int32_t *level;
-    uint32_t *bits;  // vis | B0..B3
+    uint32_t *bits;  // planes vis | B0 | B1 | B2, nw words each
     Queue<OffT> qb[2];
     Ctl *ctl;
     hbfs_layer_row *rows;
@@ -119,12 +119,18 @@ struct St {
     int dir, kind;
 };
 
+struct EnqSmem {
+    unsigned long long wtot[kBlock / 32];
+    unsigned long long wbase[kBlock / 32];
+};
+
 template <typename OffT>
 struct TdSmem {
     OffT off[kTdChunk + 2];
     OffT rs[kTdChunk + 2];
     uint32_t u[kTdChunk + 2];
     int64_t q0, cnt;
+    EnqSmem enq;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -144,21 +150,33 @@ __device__ __forceinline__ int64_t last_le(const OffT *a, int64_t len, uint64_t 
     return lo;
 }
 
-__device__ __forceinline__ bool test_bit(const uint32_t *bm, uint32_t a) {
+// A bitmap plane (LSB-first words).  Planes are separate arrays: interleaving
+// them per word was measured slower (the frontier plane's L1/L2 footprint grows
+// 4x and bottom-up probes lose locality).
+struct Plane {
+    uint32_t *p;
+    __device__ __forceinline__ uint32_t &operator[](int64_t w) const { return p[w]; }
+};
+
+__device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
     return (bm[a >> 5] >> (a & 31)) & 1u;
 }
 
-// Warp-aggregated append to a queue: every lane contributes up to I entries
-// (v, deg, row start).  One 64-bit atomic per warp reserves both the queue slots
-// and the arc range (count<<35 | degree sum), so queue order and arc-prefix
-// order agree.  The warp also records, for every top-down chunk boundary
-// c*kTdChunk inside its arc range, the queue slot that holds it — the top-down
-// phase then needs no search to start a chunk.
+// Block-aggregated append to a queue: every thread contributes up to I entries
+// (v, deg, row start).  Warps scan their lanes, the CTA scans its warps, and ONE
+// 64-bit atomic per CTA reserves both the queue slots and the arc range
+// (count<<35 | degree sum), so queue order and arc-prefix order agree and the
+// global counter sees one atomic per CTA work item, not one per warp.  Each
+// warp also records, for every top-down chunk boundary c*kTdChunk inside its
+// arc range, the queue slot holding it — the top-down phase then needs no
+// search to start a chunk.  Must be called by every thread of the CTA.
 template <typename OffT, int I>
-__device__ __forceinline__ void warp_enqueue(const bool (&claim)[I], const uint32_t (&v)[I],
-                                             const uint64_t (&deg)[I], const OffT (&rsv)[I],
-                                             unsigned long long *counter, const Queue<OffT> &Q) {
+__device__ __forceinline__ void block_enqueue(const bool (&claim)[I], const uint32_t (&v)[I],
+                                              const uint64_t (&deg)[I], const OffT (&rsv)[I],
+                                              unsigned long long *counter, const Queue<OffT> &Q,
+                                              EnqSmem &es) {
     const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t cl = 0;
     uint64_t dl = 0;
 #pragma unroll
@@ -166,9 +184,6 @@ __device__ __forceinline__ void warp_enqueue(const bool (&claim)[I], const uint3
         cl += claim[k] ? 1u : 0u;
         dl += claim[k] ? deg[k] : 0ull;
     }
-    const unsigned m = __ballot_sync(full, cl != 0);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
     uint32_t ci = cl;
     uint64_t di = dl;
 #pragma unroll
@@ -180,13 +195,23 @@ __device__ __forceinline__ void warp_enqueue(const bool (&claim)[I], const uint3
             di += yd;
         }
     }
-    const uint64_t totc = __shfl_sync(full, ci, 31);
-    const uint64_t totd = __shfl_sync(full, di, 31);
-    const int leader = __ffs(m) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(counter, (totc << kPackShift) + totd);
-    base = __shfl_sync(full, base, leader);
+    if (lane == 31) es.wtot[wid] = ((unsigned long long)ci << kPackShift) + di;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const unsigned long long t = es.wtot[w];
+            es.wtot[w] = run;  // exclusive, packed
+            run += t;
+        }
+        es.wbase[0] = run ? atomicAdd(counter, run) : 0ull;
+    }
+    __syncthreads();
+    const unsigned long long wtot = __shfl_sync(full, ((unsigned long long)ci << kPackShift) + di, 31);
+    if (wtot == 0) return;
+    const unsigned long long base = es.wbase[0] + es.wtot[wid];
     const uint64_t qb = base >> kPackShift, db = base & kPackMask;
+    const uint64_t totd = wtot & kPackMask;
     {
         uint64_t pos = qb + ci - cl, off = db + di - dl;
 #pragma unroll
@@ -247,7 +272,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // step, lowest position winning (ballot + ffs) — the reference's first-hit rule
 // (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
 template <typename OffT, int K>
-__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const uint32_t *bm,
+__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const Plane bm,
                                            const bool (&act)[K], const OffT (&s)[K],
                                            const OffT (&e)[K], int64_t (&hit)[K],
                                            uint32_t (&hu)[K]) {
@@ -357,10 +382,10 @@ __device__ void phase_init(const Args<OffT> &A) {
         A.parent[i] = r ? root : HBFS_NIL;
         A.level[i] = r ? 0 : -1;
     }
-    // vis and B0 hold the root; B1..B3 zero
+    // vis and B0 hold the root; B1, B2 zero
     const int64_t rw = root >> 5;
     const uint32_t rb = 1u << (root & 31);
-    for (int64_t w = tid; w < 5 * A.nw; w += nth)
+    for (int64_t w = tid; w < 4 * A.nw; w += nth)
         A.bits[w] = (w == rw || w == A.nw + rw) ? rb : 0u;
     const OffT r0 = __ldg(A.rs + root);
     const uint64_t rdeg = (uint64_t)(__ldg(A.rs + root + 1) - r0);
@@ -388,14 +413,14 @@ __device__ void phase_init(const Args<OffT> &A) {
 // atomic.  Replaces top_down_layer / top_down_chunked (_native.pyx:65-86,
 // :207-239).
 template <typename OffT>
-__device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, uint32_t *out,
-                         uint32_t *spare, Ctr *ctr, TdSmem<OffT> &sm) {
+__device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
+                         const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
     constexpr int I = kTdItems;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
-    uint32_t *vis = A.bits;
+    const Plane vis{A.bits};
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
     const int32_t depth1 = (int32_t)S.layer + 1;
@@ -403,8 +428,8 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, u
 
     for (int64_t w = tid; w < A.nw; w += nth) spare[w] = 0;
     if (!any_parent) {
-        // min-id mode keeps vis = "visited before the layer"; commit the
-        // frontier now (the tests below use vis | in, so no barrier is needed)
+        // min-id mode lets vis lag by the frontier; commit it now (the tests
+        // below use vis | in, so no barrier is needed)
         for (int64_t i = tid; i < nf; i += nth) {
             const uint32_t x = Q.q[i];
             atomicOr(&vis[x >> 5], 1u << (x & 31));
@@ -458,7 +483,8 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, u
             }
         }
         if (any_parent) {
-            // claim on the visited bitmap itself: one L2 load per arc
+            // first claimer wins: claim on the visited bitmap itself (one L2
+            // load per arc), the claimer also sets the next-frontier bit
 #pragma unroll
             for (int k = 0; k < I; ++k) vw[k] = ok[k] ? vis[v[k] >> 5] : ~0u;
 #pragma unroll
@@ -466,11 +492,12 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, u
                 const uint32_t b = 1u << (v[k] & 31);
                 claim[k] = false;
                 if (!(vw[k] & b)) claim[k] = !(atomicOr(&vis[v[k] >> 5], b) & b);
+                if (claim[k]) atomicOr(&out[v[k] >> 5], b);
             }
         } else {
             // min-id parents: every arc into a vertex unvisited before the layer
-            // takes part in an atomicMin, so `visited` must mean "before this
-            // layer" (vis | in); claims go to `out`.
+            // takes part in an atomicMin, so `visited` means "before this layer"
+            // (vis | in) and claims go to `out`.
             uint32_t ow[I];
 #pragma unroll
             for (int k = 0; k < I; ++k) {
@@ -494,16 +521,13 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, u
             deg[k] = 0;
             rsv[k] = 0;
             if (claim[k]) {
-                if (any_parent) {
-                    atomicOr(&out[v[k] >> 5], 1u << (v[k] & 31));
-                    A.parent[v[k]] = u[k];
-                }
+                if (any_parent) A.parent[v[k]] = u[k];
                 A.level[v[k]] = depth1;
                 rsv[k] = __ldg(A.rs + v[k]);
                 deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - rsv[k]);
             }
         }
-        warp_enqueue<OffT, I>(claim, v, deg, rsv, &ctr->packed, NQ);
+        block_enqueue<OffT, I>(claim, v, deg, rsv, &ctr->packed, NQ, sm.enq);
         __syncthreads();
     }
 }
@@ -520,14 +544,14 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const uint32_t *in, u
 // bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
 // bu_probe.h:22-106).
 template <typename OffT, int C>
-__device__ void phase_bu(const Args<OffT> &A, const St &S, const uint32_t *in, uint32_t *out,
-                         uint32_t *spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
+__device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
+                         const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = tid >> 5, nwarps = nth >> 5;
-    uint32_t *vis = A.bits;
+    const Plane vis{A.bits};
     const int32_t depth1 = (int32_t)S.layer + 1;
     const int64_t max_pos = A.max_pos;
     // packed per-thread counters: found<<35 | their degree sum ; fallbacks<<35 | gathers
@@ -540,7 +564,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const uint32_t *in, u
         const uint32_t vis0 = valid ? vis[wl] : ~0u;
         const uint32_t inl = valid ? in[wl] : 0u;
         const uint32_t pwl = valid ? __ldg(A.posw + wl) : 0u;
-        if (valid) spare[wl] = 0;
+        if (valid) spare[wl] = 0u;
         const uint32_t vwl = vis0 | inl;
         const uint32_t candl = ~vwl & pwl;
         if (valid && vwl != vis0) vis[wl] = vwl;  // commit a lagging frontier
@@ -631,32 +655,41 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const uint32_t *in, u
 }
 
 // Bitmap -> queue (with arc prefix, row starts, chunk starts) at a bottom-up ->
-// top-down switch.
+// top-down switch.  Thread per frontier word; each round every thread peels up
+// to kConvI vertices off its word and the CTA appends them with one atomic.
+constexpr int kConvI = 4;
+
 template <typename OffT>
-__device__ void phase_convert(const Args<OffT> &A, const St &S, const uint32_t *in) {
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
+__device__ void phase_convert(const Args<OffT> &A, const St &S, const Plane in, EnqSmem &es) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
-    for (int64_t w0 = tid - lane; w0 < A.nw; w0 += nth) {
-        const int64_t w = w0 + lane;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
+        const int64_t w = w0 + threadIdx.x;
         uint32_t bits = w < A.nw ? in[w] : 0u;
-        while (__any_sync(0xffffffffu, bits != 0)) {
-            const bool has = bits != 0;
-            uint32_t v = 0;
-            uint64_t deg = 0;
-            OffT r0 = 0;
-            if (has) {
-                v = (uint32_t)(w * 32 + __ffs(bits) - 1);
-                bits &= bits - 1;
-                r0 = __ldg(A.rs + v);
-                deg = (uint64_t)(__ldg(A.rs + v + 1) - r0);
+        while (__syncthreads_or(bits != 0)) {
+            bool has[kConvI];
+            uint32_t v[kConvI];
+            uint64_t deg[kConvI];
+            OffT r0[kConvI];
+#pragma unroll
+            for (int k = 0; k < kConvI; ++k) {
+                has[k] = bits != 0;
+                v[k] = 0;
+                deg[k] = 0;
+                r0[k] = 0;
+                if (has[k]) {
+                    v[k] = (uint32_t)(w * 32 + __ffs(bits) - 1);
+                    bits &= bits - 1;
+                }
             }
-            const bool hk[1] = {has};
-            const uint32_t vk[1] = {v};
-            const uint64_t dk[1] = {deg};
-            const OffT rk[1] = {r0};
-            warp_enqueue<OffT, 1>(hk, vk, dk, rk, &A.ctl->conv, Q);
+#pragma unroll
+            for (int k = 0; k < kConvI; ++k) {
+                if (has[k]) {
+                    r0[k] = __ldg(A.rs + v[k]);
+                    deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - r0[k]);
+                }
+            }
+            block_enqueue<OffT, kConvI>(has, v, deg, r0, &A.ctl->conv, Q, es);
         }
     }
 }
@@ -702,13 +735,11 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         int64_t fv, gv;
         const int dir = decide(A.H, S.dir, S.v_f, S.e_f, S.eu_v, S.eu_e, S.prev_vf, &fv, &gv);
         const int64_t L = S.layer;
-        uint32_t *B = A.bits + A.nw;
-        const uint32_t *in = B + A.nw * (L % 4);
-        uint32_t *out = B + A.nw * ((L + 1) % 4);
-        uint32_t *spare = B + A.nw * ((L + 2) % 4);
+        const Plane in{A.bits + A.nw * (1 + L % 3)}, out{A.bits + A.nw * (1 + (L + 1) % 3)},
+            spare{A.bits + A.nw * (1 + (L + 2) % 3)};
         Ctr *ctr = &A.ctl->ctr[L % 3];
         if (dir == HBFS_TOP_DOWN && S.kind == 1) {
-            phase_convert(A, S, in);
+            phase_convert(A, S, in, sm.enq);
             grid.sync();
         }
         // Slot (L+1)%3 was last read right after the barrier that ended layer
@@ -836,7 +867,7 @@ static int ws_alloc(hbfs_graph *g) {
     if (!rc) rc = w->parent.alloc(n * 4);
     if (!rc) rc = w->level.alloc(n * 4);
     w->ncs = g->arcs / kTdChunk + 2;
-    if (!rc) rc = w->bits.alloc(5 * nw * 4 + 16);
+    if (!rc) rc = w->bits.alloc(4 * nw * 4 + 64);
     if (!rc) rc = w->q.alloc(2 * (n + 1) * 4 + 16);
     if (!rc) rc = w->qo.alloc(2 * (n + 1) * sizeof(OffT));
     if (!rc) rc = w->qr.alloc(2 * (n + 1) * sizeof(OffT));

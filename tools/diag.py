@@ -12,13 +12,14 @@ ap.add_argument("--roots", type=int, default=8)
 ap.add_argument("--heuristic", default="beamer")
 ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--parent-mode", default="minid")
+ap.add_argument("--root", type=int, default=-1)
 a = ap.parse_args()
 probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
 t0 = time.time()
 g = hb.generate_graph(hb.GraphParams(scale=a.scale, edgefactor=16, seed=1, probs=probs))
 torch.cuda.synchronize()
 print(f"graph S{a.scale}: n={g.num_vertices} arcs={g.num_arcs} maxdeg={g.max_degree} wide={g.wide_offsets} build {time.time()-t0:.2f}s", flush=True)
-roots = hb.sample_sources(g, 64, 1)[: a.roots]
+roots = hb.sample_sources(g, 64, 1)[: a.roots] if a.root < 0 else [a.root] * a.roots
 p = hb.HeuristicParams(alpha=14, beta=24, heuristic=a.heuristic, counter_mode="edge")
 n = g.num_vertices
 par = torch.empty(n, dtype=torch.int32, device="cuda"); lev = torch.empty_like(par)
