@@ -45,6 +45,13 @@ constexpr int kLaneVecs = 2;                 // uint4 probes per lane before the
 constexpr int kPackShift = 35;               // packed counter: count<<35 | degree sum
 constexpr unsigned long long kPackMask = (1ull << kPackShift) - 1;
 constexpr int64_t kRowsCap = 1024;           // trace rows per launch
+// Column-blocked top-down (hub frontiers): frontier rows are split into
+// kCb ranges of target ids and processed range by range so the active slice
+// of parent/level/bitmaps/row-starts stays L2-resident.
+constexpr int kCbMaxRanges = 32;
+constexpr int64_t kCbMaxF = 65536;           // frontier entries eligible for blocking
+constexpr int64_t kCbMinArcs = int64_t(1) << 21;
+constexpr int64_t kCbMinN = int64_t(1) << 23;
 
 struct Ctr {
     unsigned long long packed;  // discovered count << 35 | their degree sum
@@ -61,6 +68,7 @@ struct Ctl {
     int64_t rows;               // rows written by the last launch
     unsigned long long conv;    // enqueue counter of the bitmap->queue phase
     Ctr ctr[3];
+    unsigned long long cbctr[2][kCbMaxRanges];  // per-range segment counters (2 banks)
 };
 
 struct Heur {
@@ -106,6 +114,9 @@ struct Args {
     int32_t *level;
     uint32_t *bits;  // planes vis | B0 | B1 | B2, nw words each
     Queue<OffT> qb[2];
+    Queue<OffT> cbq;  // per-range segment queues: entries r*cb_max_f.., chunk starts r*cb_cs_stride..
+    int cb_ranges;
+    int64_t cb_range_len, cb_cs_stride, cb_min_arcs;
     Ctl *ctl;
     hbfs_layer_row *rows;
     int64_t rows_cap;
@@ -397,6 +408,8 @@ __device__ void phase_init(const Args<OffT> &A) {
         A.qb[0].qr[0] = r0;
         Ctl *c = A.ctl;
         for (int s = 0; s < 3; ++s) c->ctr[s] = Ctr{0, 0, 0, 0};
+        for (int b = 0; b < 2; ++b)
+            for (int r = 0; r < kCbMaxRanges; ++r) c->cbctr[b][r] = 0;
         c->conv = 0;
         c->done = 0;
     }
@@ -412,32 +425,37 @@ __device__ void phase_init(const Args<OffT> &A) {
 // the claimer stamps the level and the warp enqueues all its claims with one
 // atomic.  Replaces top_down_layer / top_down_chunked (_native.pyx:65-86,
 // :207-239).
+// Prologue of every top-down layer: clear the spare bitmap; in min-id mode
+// commit the frontier to vis (the arc tests use vis | in, so no barrier).
 template <typename OffT>
-__device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
-                         const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
-    constexpr int I = kTdItems;
+__device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const Queue<OffT> &Q = A.qb[S.layer & 1];
-    const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
     const Plane vis{A.bits};
-    const int64_t nf = S.v_f;
-    const uint64_t mf = (uint64_t)S.e_f;
-    const int32_t depth1 = (int32_t)S.layer + 1;
-    const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
-
     for (int64_t w = tid; w < A.nw; w += nth) spare[w] = 0;
-    if (!any_parent) {
-        // min-id mode lets vis lag by the frontier; commit it now (the tests
-        // below use vis | in, so no barrier is needed)
-        for (int64_t i = tid; i < nf; i += nth) {
+    if (A.parent_mode != HBFS_PARENT_ANY) {
+        for (int64_t i = tid; i < S.v_f; i += nth) {
             const uint32_t x = Q.q[i];
             atomicOr(&vis[x >> 5], 1u << (x & 31));
         }
     }
+}
 
-    const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+// One CTA work item of a top-down layer: kTdChunk consecutive arcs (chunk c of
+// nchunks) of the concatenated rows of queue Q (nf entries, mf arcs).  Each
+// thread maps its kTdItems arcs to (u, position) by binary search in the CTA's
+// shared-memory slice of the degree prefix; the items are staged (all
+// adjacency loads, then all visited-bit loads, then all claims) so their
+// memory latencies overlap; claims are appended to NQ with one atomic per CTA.
+template <typename OffT>
+__device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
+                                         uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
+                                         const Plane in, const Plane out, const Queue<OffT> &NQ,
+                                         Ctr *ctr, TdSmem<OffT> &sm) {
+    constexpr int I = kTdItems;
+    const Plane vis{A.bits};
+    const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
         const uint64_t a0 = (uint64_t)c * kTdChunk;
         const uint64_t a1 = min(a0 + (uint64_t)kTdChunk, mf);
         if (threadIdx.x == 0) {
@@ -529,6 +547,110 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
         }
         block_enqueue<OffT, I>(claim, v, deg, rsv, &ctr->packed, NQ, sm.enq);
         __syncthreads();
+}
+
+// Top-down layer: arc-balanced expansion of the frontier queue (hubs of any
+// degree spread over many CTAs, coalesced adjacency reads).  A claim is one
+// atomicOr on an L2-resident bitmap; min-id mode adds atomicMin(parent) for
+// every arc into a vertex unvisited before the layer.  Replaces
+// top_down_layer / top_down_chunked (_native.pyx:65-86, :207-239).
+template <typename OffT>
+__device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
+                         const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
+    const Queue<OffT> &Q = A.qb[S.layer & 1];
+    const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
+    td_prologue(A, S, spare);
+    const int64_t nf = S.v_f;
+    const uint64_t mf = (uint64_t)S.e_f;
+    const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
+        td_chunk(A, Q, nf, mf, c, nchunks, (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
+}
+
+template <typename OffT>
+__device__ __forceinline__ Queue<OffT> cb_queue(const Args<OffT> &A, int r, int64_t cb_max_f) {
+    Queue<OffT> q;
+    q.q = A.cbq.q + r * cb_max_f;
+    q.qo = A.cbq.qo + r * cb_max_f;
+    q.qr = A.cbq.qr + r * cb_max_f;
+    q.cs = A.cbq.cs + r * A.cb_cs_stride;
+    return q;
+}
+
+// Column-blocked top-down, phase A: split every frontier row into cb_ranges
+// sub-rows by target id (rows are sorted, so each is a contiguous segment
+// found by binary search) and append the segments to per-range queues.
+template <typename OffT>
+__device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spare, int bank) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const Queue<OffT> &Q = A.qb[S.layer & 1];
+    td_prologue(A, S, spare);
+    const int P = A.cb_ranges;
+    const int64_t nf = S.v_f;
+    const uint64_t mf = (uint64_t)S.e_f;
+    for (int64_t i = tid >> 5; i < nf; i += nth >> 5) {
+        const uint32_t u = Q.q[i];
+        const OffT s = Q.qr[i];
+        const uint64_t o = (uint64_t)Q.qo[i];
+        const uint64_t deg = ((i + 1 < nf) ? (uint64_t)Q.qo[i + 1] : mf) - o;
+        // lane r: b_r = first row position with target >= r * range_len
+        uint64_t b = 0;
+        if (lane >= P) b = deg;
+        else if (lane > 0) {
+            const uint64_t key = (uint64_t)lane * (uint64_t)A.cb_range_len;
+            uint64_t lo = 0, hi = deg;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if ((uint64_t)__ldg(A.adj + (uint64_t)s + mid) < key) lo = mid + 1; else hi = mid;
+            }
+            b = lo;
+        }
+        const uint64_t bn = __shfl_down_sync(0xffffffffu, b, 1);
+        if (lane < P && bn > b) {
+            const uint64_t len = bn - b;
+            const unsigned long long old =
+                atomicAdd(&A.ctl->cbctr[bank][lane], (1ull << kPackShift) + len);
+            const uint64_t pos = old >> kPackShift, db = old & kPackMask;
+            const Queue<OffT> R = cb_queue(A, lane, kCbMaxF);
+            R.q[pos] = u;
+            R.qo[pos] = (OffT)db;
+            R.qr[pos] = (OffT)((uint64_t)s + b);
+            for (uint64_t c = (db + kTdChunk - 1) / kTdChunk; c * kTdChunk < db + len; ++c)
+                R.cs[c] = (uint32_t)pos;
+        }
+    }
+}
+
+// Column-blocked top-down, phase B: all CTAs walk the chunks of range 0, then
+// range 1, ... (one global chunk index space), so the frontier's arcs hit one
+// target range at a time.
+template <typename OffT>
+__device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
+                             Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre) {
+    const int P = A.cb_ranges;
+    const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int r = 0; r < P; ++r) {
+            s_pre[r] = run;
+            const unsigned long long t = __ldcg(&A.ctl->cbctr[bank][r]);
+            run += (int64_t)(((t & kPackMask) + kTdChunk - 1) / kTdChunk);
+        }
+        s_pre[P] = run;
+    }
+    __syncthreads();
+    const int64_t total = s_pre[P];
+    int r = 0;
+    for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
+        while (g >= s_pre[r + 1]) ++r;
+        const unsigned long long t = __ldcg(&A.ctl->cbctr[bank][r]);
+        const int64_t nf_r = (int64_t)(t >> kPackShift);
+        const uint64_t mf_r = t & kPackMask;
+        const Queue<OffT> R = cb_queue(A, r, kCbMaxF);
+        td_chunk(A, R, nf_r, mf_r, g - s_pre[r], s_pre[r + 1] - s_pre[r], (int32_t)S.layer + 1,
+                 in, out, NQ, ctr, sm);
     }
 }
 
@@ -702,6 +824,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     __shared__ TdSmem<OffT> sm;
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];  // per warp: found bits of its 32-word tile
+    __shared__ int64_t s_pre[kCbMaxRanges + 1];
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
 
     St S;
@@ -742,13 +865,21 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             phase_convert(A, S, in, sm.enq);
             grid.sync();
         }
+        const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && S.e_f >= A.cb_min_arcs &&
+                        S.v_f <= kCbMaxF;
         // Slot (L+1)%3 was last read right after the barrier that ended layer
         // L-2, so every CTA is past that read; it must be zero when layer L+1
         // starts accumulating.  The conversion counter is free again too.
         if (leader) {
             A.ctl->ctr[(L + 1) % 3] = Ctr{0, 0, 0, 0};
             A.ctl->conv = 0;
+            for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
+        if (cb) {
+            phase_cb_build(A, S, spare, (int)(L & 1));
+            grid.sync();
+            phase_cb_run(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
+        } else
         if (dir == HBFS_TOP_DOWN) phase_td(A, S, in, out, spare, ctr, sm);
         else phase_bu<OffT, K>(A, S, in, out, spare, ctr, red, s_found + (threadIdx.x & ~31));
         grid.sync();
@@ -832,6 +963,11 @@ constexpr int kDefaultVariant = 0;
 // Measured on B200 (tools/diag.py sweeps): small graphs are latency-bound and
 // prefer one fat CTA per SM with 4 searches in flight per lane (variant 4);
 // SCALE >= 24 prefers two CTAs per SM with 2 searches per lane (variant 3).
+static int64_t env_i64(const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    return e ? atoll(e) : dflt;
+}
+
 static int variant_index(int64_t n) {
     const char *e = getenv("HBFS_KERNEL_VARIANT");
     if (e) return atoi(e);
@@ -844,6 +980,8 @@ struct Workspace {
     int64_t n = 0;
     int wide = 0;
     DevBuf parent, level, bits, q, qo, qr, cs, ctl;  // ctl: Ctl followed by kRowsCap rows
+    DevBuf cbq, cbqo, cbqr, cbcs;  // column-blocked top-down segment queues
+    int cb_ranges = 0;
     int64_t ncs = 0;  // chunk-start entries per queue buffer
     int grid = 0;
     const void *fn = nullptr;
@@ -872,6 +1010,18 @@ static int ws_alloc(hbfs_graph *g) {
     if (!rc) rc = w->qo.alloc(2 * (n + 1) * sizeof(OffT));
     if (!rc) rc = w->qr.alloc(2 * (n + 1) * sizeof(OffT));
     if (!rc) rc = w->cs.alloc(2 * w->ncs * 4);
+    // column blocking for graphs whose parent/level arrays exceed L2
+    // (HBFS_CB_MIN_N / HBFS_CB_RANGES: test knobs that force blocking on small graphs)
+    const int64_t cb_min_n = env_i64("HBFS_CB_MIN_N", kCbMinN);
+    w->cb_ranges = n >= cb_min_n ? (int)std::min<int64_t>(31, std::max<int64_t>(2, n >> 22)) : 0;
+    if (w->cb_ranges) w->cb_ranges = (int)std::min<int64_t>(31, env_i64("HBFS_CB_RANGES", w->cb_ranges));
+    if (!rc && w->cb_ranges) {
+        const int64_t P = w->cb_ranges;
+        rc = w->cbq.alloc(P * kCbMaxF * 4);
+        if (!rc) rc = w->cbqo.alloc(P * kCbMaxF * sizeof(OffT));
+        if (!rc) rc = w->cbqr.alloc(P * kCbMaxF * sizeof(OffT));
+        if (!rc) rc = w->cbcs.alloc(P * w->ncs * 4);
+    }
     if (!rc) rc = w->ctl.alloc(ctl_bytes());
     if (!rc && cudaMallocHost(&w->h_ctl, ctl_bytes()) != cudaSuccess)
         rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
@@ -919,6 +1069,14 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.level = (dev_out && level) ? level : w->level.as<int32_t>();
     A.bits = w->bits.as<uint32_t>();
     A.ncs = w->ncs;
+    A.cb_ranges = w->cb_ranges;
+    A.cb_range_len = w->cb_ranges ? (g->n + w->cb_ranges - 1) / w->cb_ranges : 0;
+    A.cb_cs_stride = w->ncs;
+    A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
+    A.cbq.q = w->cbq.as<uint32_t>();
+    A.cbq.qo = w->cbqo.as<OffT>();
+    A.cbq.qr = w->cbqr.as<OffT>();
+    A.cbq.cs = w->cbcs.as<uint32_t>();
     for (int b = 0; b < 2; ++b) {
         A.qb[b].q = w->q.as<uint32_t>() + b * (g->n + 1);
         A.qb[b].qo = w->qo.as<OffT>() + b * (g->n + 1);

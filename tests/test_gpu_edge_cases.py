@@ -172,3 +172,37 @@ def test_reference_csr_import(cuda, oracle):
     tree, trace = hb.hybrid_bfs(host, 7)  # any object with the reference CsrGraph fields
     par, lev, rows = oracle.hybrid_bfs(host, 7)
     assert np.array_equal(tree.parent, par) and len(trace) == len(rows)
+
+
+def test_column_blocked_top_down_forced(cuda, oracle, small_golden, golden_hashes):
+    """Force the column-blocked top-down path (normally SCALE >= 23 hub layers)
+    on the golden small graphs: every top-down layer is split into target ranges.
+    Results must not change (levels, min-id parents, traces)."""
+    import os
+
+    hb = cuda
+    old = {k: os.environ.get(k) for k in ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES")}
+    os.environ.update(HBFS_CB_MIN_N="0", HBFS_CB_MIN_ARCS="0", HBFS_CB_RANGES="7")
+    try:
+        for meta in golden_hashes["small"]:
+            name = meta["name"]
+            p = dict(meta["params"])
+            if "probs" in p:
+                p["probs"] = tuple(p["probs"])
+            g = hb.generate_graph(hb.GraphParams(**p))  # fresh workspace reads the knobs
+            for s in small_golden[f"{name}/sources"][:4]:
+                s = int(s)
+                for mode, kw in (("simd_default", dict(use_simd=True)),
+                                 ("force_td", dict(use_simd=False, force_direction="top-down"))):
+                    r = hb.bfs(g, s, device=False, **kw)
+                    assert np.array_equal(r.level, small_golden[f"{name}/{s}/level"]), (name, s, mode)
+                    assert np.array_equal(r.parent, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
+                ra = hb.bfs(g, s, device=False, parent_mode="any", force_direction="top-down")
+                assert np.array_equal(ra.level, small_golden[f"{name}/{s}/level"])
+                assert hb.validate_tree(g, s, ra.parent, ra.level).ok
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
