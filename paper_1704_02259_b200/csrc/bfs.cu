@@ -52,6 +52,9 @@ constexpr int kCbMaxRanges = 32;
 constexpr int64_t kCbMaxF = 65536;           // frontier entries eligible for blocking
 constexpr int64_t kCbMinArcs = int64_t(1) << 21;
 constexpr int64_t kCbMinN = int64_t(1) << 23;
+// Top-down layers with at least this many frontier arcs expand fire-and-forget
+// and harvest the next frontier from its bitmap (one extra barrier).
+constexpr int64_t kHarvestMinArcs = int64_t(1) << 22;
 
 struct Ctr {
     unsigned long long packed;  // discovered count << 35 | their degree sum
@@ -116,7 +119,7 @@ struct Args {
     Queue<OffT> qb[2];
     Queue<OffT> cbq;  // per-range segment queues: entries r*cb_max_f.., chunk starts r*cb_cs_stride..
     int cb_ranges;
-    int64_t cb_range_len, cb_cs_stride, cb_min_arcs;
+    int64_t cb_range_len, cb_cs_stride, cb_min_arcs, harvest_min_arcs;
     Ctl *ctl;
     hbfs_layer_row *rows;
     int64_t rows_cap;
@@ -448,7 +451,11 @@ __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare)
 // shared-memory slice of the degree prefix; the items are staged (all
 // adjacency loads, then all visited-bit loads, then all claims) so their
 // memory latencies overlap; claims are appended to NQ with one atomic per CTA.
-template <typename OffT>
+// Harvest=true (large layers): pure fire-and-forget expansion — every arc into
+// a vertex unvisited before the layer does RED.OR on its next-frontier bit and
+// RED.MIN (min-id) or a plain store (any) on its parent; levels, counters and
+// the next queue come from a word-order harvest of the bitmap afterwards.
+template <typename OffT, bool Harvest>
 __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
                                          uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
                                          const Plane in, const Plane out, const Queue<OffT> &NQ,
@@ -500,7 +507,24 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
                 v[k] = __ldg(A.adj + (uint64_t)rsu + (a - (uint64_t)off));
             }
         }
-        if (any_parent) {
+        if (Harvest) {
+            uint32_t ow[I];
+#pragma unroll
+            for (int k = 0; k < I; ++k) {
+                vw[k] = ok[k] ? (__ldg(&vis[v[k] >> 5]) | __ldg(&in[v[k] >> 5])) : ~0u;
+                ow[k] = ok[k] ? out[v[k] >> 5] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < I; ++k) {
+                const uint32_t b = 1u << (v[k] & 31);
+                if (!(vw[k] & b)) {
+                    if (!(ow[k] & b)) atomicOr(&out[v[k] >> 5], b);
+                    if (any_parent) A.parent[v[k]] = u[k];
+                    else atomicMin(&A.parent[v[k]], u[k]);
+                }
+            }
+            return;
+        } else if (any_parent) {
             // first claimer wins: claim on the visited bitmap itself (one L2
             // load per arc), the claimer also sets the next-frontier bit
 #pragma unroll
@@ -554,7 +578,7 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
 // atomicOr on an L2-resident bitmap; min-id mode adds atomicMin(parent) for
 // every arc into a vertex unvisited before the layer.  Replaces
 // top_down_layer / top_down_chunked (_native.pyx:65-86, :207-239).
-template <typename OffT>
+template <typename OffT, bool Harvest>
 __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
@@ -564,7 +588,7 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
     const uint64_t mf = (uint64_t)S.e_f;
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
-        td_chunk(A, Q, nf, mf, c, nchunks, (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
+        td_chunk<OffT, Harvest>(A, Q, nf, mf, c, nchunks, (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
 }
 
 template <typename OffT>
@@ -626,7 +650,7 @@ __device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spa
 // Column-blocked top-down, phase B: all CTAs walk the chunks of range 0, then
 // range 1, ... (one global chunk index space), so the frontier's arcs hit one
 // target range at a time.
-template <typename OffT>
+template <typename OffT, bool Harvest>
 __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                              Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre) {
     const int P = A.cb_ranges;
@@ -649,7 +673,7 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
         const int64_t nf_r = (int64_t)(t >> kPackShift);
         const uint64_t mf_r = t & kPackMask;
         const Queue<OffT> R = cb_queue(A, r, kCbMaxF);
-        td_chunk(A, R, nf_r, mf_r, g - s_pre[r], s_pre[r + 1] - s_pre[r], (int32_t)S.layer + 1,
+        td_chunk<OffT, Harvest>(A, R, nf_r, mf_r, g - s_pre[r], s_pre[r + 1] - s_pre[r], (int32_t)S.layer + 1,
                  in, out, NQ, ctr, sm);
     }
 }
@@ -782,12 +806,15 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
 constexpr int kConvI = 4;
 
 template <typename OffT>
-__device__ void phase_convert(const Args<OffT> &A, const St &S, const Plane in, EnqSmem &es) {
-    const Queue<OffT> &Q = A.qb[S.layer & 1];
+__device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const Plane bm,
+                              unsigned long long *counter, int32_t stamp_level, bool commit_vis,
+                              EnqSmem &es) {
+    const Plane vis{A.bits};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
         const int64_t w = w0 + threadIdx.x;
-        uint32_t bits = w < A.nw ? in[w] : 0u;
+        uint32_t bits = w < A.nw ? bm[w] : 0u;
+        if (commit_vis && bits) vis[w] |= bits;
         while (__syncthreads_or(bits != 0)) {
             bool has[kConvI];
             uint32_t v[kConvI];
@@ -809,9 +836,10 @@ __device__ void phase_convert(const Args<OffT> &A, const St &S, const Plane in, 
                 if (has[k]) {
                     r0[k] = __ldg(A.rs + v[k]);
                     deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - r0[k]);
+                    if (stamp_level) A.level[v[k]] = stamp_level;
                 }
             }
-            block_enqueue<OffT, kConvI>(has, v, deg, r0, &A.ctl->conv, Q, es);
+            block_enqueue<OffT, kConvI>(has, v, deg, r0, counter, Q, es);
         }
     }
 }
@@ -862,7 +890,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             spare{A.bits + A.nw * (1 + (L + 2) % 3)};
         Ctr *ctr = &A.ctl->ctr[L % 3];
         if (dir == HBFS_TOP_DOWN && S.kind == 1) {
-            phase_convert(A, S, in, sm.enq);
+            phase_convert(A, A.qb[L & 1], in, &A.ctl->conv, 0, false, sm.enq);
             grid.sync();
         }
         const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && S.e_f >= A.cb_min_arcs &&
@@ -875,13 +903,22 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             A.ctl->conv = 0;
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
+        const bool harvest = dir == HBFS_TOP_DOWN && S.e_f >= A.harvest_min_arcs;
         if (cb) {
             phase_cb_build(A, S, spare, (int)(L & 1));
             grid.sync();
-            phase_cb_run(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
-        } else
-        if (dir == HBFS_TOP_DOWN) phase_td(A, S, in, out, spare, ctr, sm);
-        else phase_bu<OffT, K>(A, S, in, out, spare, ctr, red, s_found + (threadIdx.x & ~31));
+            if (harvest) phase_cb_run<OffT, true>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
+            else phase_cb_run<OffT, false>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
+        } else if (dir == HBFS_TOP_DOWN) {
+            if (harvest) phase_td<OffT, true>(A, S, in, out, spare, ctr, sm);
+            else phase_td<OffT, false>(A, S, in, out, spare, ctr, sm);
+        }
+        if (harvest) {
+            grid.sync();
+            phase_convert(A, A.qb[(L + 1) & 1], out, &ctr->packed, (int32_t)L + 1, true, sm.enq);
+        }
+        if (dir == HBFS_BOTTOM_UP)
+            phase_bu<OffT, K>(A, S, in, out, spare, ctr, red, s_found + (threadIdx.x & ~31));
         grid.sync();
 
         const unsigned long long packed = __ldcg(&ctr->packed);
@@ -1073,6 +1110,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.cb_range_len = w->cb_ranges ? (g->n + w->cb_ranges - 1) / w->cb_ranges : 0;
     A.cb_cs_stride = w->ncs;
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
+    A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
     A.cbq.q = w->cbq.as<uint32_t>();
     A.cbq.qo = w->cbqo.as<OffT>();
     A.cbq.qr = w->cbqr.as<OffT>();

@@ -174,15 +174,19 @@ def test_reference_csr_import(cuda, oracle):
     assert np.array_equal(tree.parent, par) and len(trace) == len(rows)
 
 
-def test_column_blocked_top_down_forced(cuda, oracle, small_golden, golden_hashes):
-    """Force the column-blocked top-down path (normally SCALE >= 23 hub layers)
-    on the golden small graphs: every top-down layer is split into target ranges.
-    Results must not change (levels, min-id parents, traces)."""
+@pytest.mark.parametrize("cb,harvest", [(True, False), (True, True), (False, True)])
+def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, cb, harvest):
+    """Force the large-layer top-down strategies on the golden small graphs:
+    column blocking (every frontier row split into target ranges, normally
+    SCALE >= 23 hub layers) and/or the harvest path (fire-and-forget expansion +
+    word-order bitmap harvest, normally m_f >= 2^18).  Results must not change."""
     import os
 
     hb = cuda
-    old = {k: os.environ.get(k) for k in ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES")}
-    os.environ.update(HBFS_CB_MIN_N="0", HBFS_CB_MIN_ARCS="0", HBFS_CB_RANGES="7")
+    keys = ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES", "HBFS_HARVEST_MIN_ARCS")
+    old = {k: os.environ.get(k) for k in keys}
+    os.environ.update(HBFS_CB_MIN_N="0" if cb else str(1 << 40), HBFS_CB_MIN_ARCS="0",
+                      HBFS_CB_RANGES="7", HBFS_HARVEST_MIN_ARCS="0" if harvest else str(1 << 40))
     try:
         for meta in golden_hashes["small"]:
             name = meta["name"]
