@@ -72,6 +72,7 @@ struct Ctl {
     unsigned long long conv;    // enqueue counter of the bitmap->queue phase
     Ctr ctr[3];
     unsigned long long cbctr[2][kCbMaxRanges];  // per-range segment counters (2 banks)
+    unsigned long long work[3];                  // dynamic work counters, slot L%3
 };
 
 struct Heur {
@@ -143,7 +144,7 @@ struct TdSmem {
     OffT off[kTdChunk + 2];
     OffT rs[kTdChunk + 2];
     uint32_t u[kTdChunk + 2];
-    int64_t q0, cnt;
+    int64_t q0, cnt, item;
     EnqSmem enq;
 };
 
@@ -171,6 +172,16 @@ struct Plane {
     uint32_t *p;
     __device__ __forceinline__ uint32_t &operator[](int64_t w) const { return p[w]; }
 };
+
+// Dynamic scheduling: every CTA first takes item blockIdx.x (no atomics, so
+// short layers pay nothing), then draws further items from a per-layer counter
+// offset past the static range.
+__device__ __forceinline__ int64_t block_grab(unsigned long long *work, int64_t *s_item) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s_item = (int64_t)gridDim.x + (int64_t)atomicAdd(work, 1ull);
+    __syncthreads();
+    return *s_item;
+}
 
 __device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
     return (bm[a >> 5] >> (a & 31)) & 1u;
@@ -410,7 +421,10 @@ __device__ void phase_init(const Args<OffT> &A) {
         A.qb[0].qo[0] = 0;
         A.qb[0].qr[0] = r0;
         Ctl *c = A.ctl;
-        for (int s = 0; s < 3; ++s) c->ctr[s] = Ctr{0, 0, 0, 0};
+        for (int s = 0; s < 3; ++s) {
+            c->ctr[s] = Ctr{0, 0, 0, 0};
+            c->work[s] = 0;
+        }
         for (int b = 0; b < 2; ++b)
             for (int r = 0; r < kCbMaxRanges; ++r) c->cbctr[b][r] = 0;
         c->conv = 0;
@@ -587,7 +601,8 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
+    unsigned long long *work = &A.ctl->work[S.layer % 3];
+    for (int64_t c = blockIdx.x; c < nchunks; c = block_grab(work, &sm.item))
         td_chunk<OffT, Harvest>(A, Q, nf, mf, c, nchunks, (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
 }
 
@@ -667,7 +682,8 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
     __syncthreads();
     const int64_t total = s_pre[P];
     int r = 0;
-    for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
+    unsigned long long *work = &A.ctl->work[S.layer % 3];
+    for (int64_t g = blockIdx.x; g < total; g = block_grab(work, &sm.item)) {
         while (g >= s_pre[r + 1]) ++r;
         const unsigned long long t = __ldcg(&A.ctl->cbctr[bank][r]);
         const int64_t nf_r = (int64_t)(t >> kPackShift);
@@ -689,6 +705,32 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
 // those of the reference's 16-lane kernel.  Replaces
 // bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
 // bu_probe.h:22-106).
+// Warp tile scheduler: a static share first (tiles warp + k*nwarps, k < kGrab:
+// no atomics, short layers spread over all warps), then dynamic grabs of kGrab
+// consecutive tiles from a per-layer counter (balances long layers).
+struct TileSched {
+    static constexpr int64_t kGrab = 4;
+    unsigned long long *work;
+    int64_t tile, nwarps, k = 0, dyn_end = -1;
+    __device__ TileSched(unsigned long long *w, int64_t warp, int64_t nw)
+        : work(w), tile(warp), nwarps(nw) {}
+    __device__ __forceinline__ int64_t next() {
+        if (dyn_end < 0) {
+            if (++k < kGrab) tile += nwarps;
+            else dyn_end = 0;
+        } else {
+            ++tile;
+        }
+        if (dyn_end >= 0 && tile >= dyn_end) {
+            unsigned long long t = 0;
+            if ((threadIdx.x & 31) == 0) t = atomicAdd(work, (unsigned long long)kGrab);
+            tile = nwarps * kGrab + (int64_t)__shfl_sync(0xffffffffu, t, 0);
+            dyn_end = tile + kGrab;
+        }
+        return tile;
+    }
+};
+
 template <typename OffT, int C>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
@@ -696,7 +738,6 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    const int64_t gwarp = tid >> 5, nwarps = nth >> 5;
     const Plane vis{A.bits};
     const int32_t depth1 = (int32_t)S.layer + 1;
     const int64_t max_pos = A.max_pos;
@@ -704,7 +745,8 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     unsigned long long c_fd = 0, c_fg = 0;
     const int64_t ntiles = (A.nw + 31) >> 5;
 
-    for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+    TileSched ts(&A.ctl->work[S.layer % 3], tid >> 5, nth >> 5);
+    for (int64_t tile = ts.tile; tile < ntiles; tile = ts.next()) {
         const int64_t wl = tile * 32 + lane;
         const bool valid = wl < A.nw;
         const uint32_t vis0 = valid ? vis[wl] : ~0u;
@@ -900,6 +942,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         // starts accumulating.  The conversion counter is free again too.
         if (leader) {
             A.ctl->ctr[(L + 1) % 3] = Ctr{0, 0, 0, 0};
+            A.ctl->work[(L + 1) % 3] = 0;
             A.ctl->conv = 0;
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
