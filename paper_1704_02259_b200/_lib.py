@@ -13,7 +13,8 @@ import os
 from .generator import CapacityError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "csrc", "libhbfs.so")
+# HBFS_LIB: experiment knob to load an alternative build of the library
+LIB_PATH = os.environ.get("HBFS_LIB") or os.path.join(PKG, "csrc", "libhbfs.so")
 
 HBFS_OK, HBFS_EINVAL, HBFS_ERANGE, HBFS_ECAPACITY, HBFS_ECUDA, HBFS_ENCCL = range(6)
 

@@ -41,7 +41,10 @@ namespace hbfs {
 
 constexpr int kTdItems = 4;
 constexpr int kTdChunk = kBlock * kTdItems;  // arcs per CTA work item
-constexpr int kLaneVecs = 2;                 // uint4 probes per lane before the warp scan
+// uint4 row probes per lane before the warp-cooperative scan: 2 normally, 4 in
+// bottom-up layers whose frontier is tiny (most rows are scanned to the end)
+constexpr int kLaneVecs = 2;
+constexpr int kLaneVecsScan = 4;
 constexpr int kPackShift = 35;               // packed counter: count<<35 | degree sum
 constexpr unsigned long long kPackMask = (1ull << kPackShift) - 1;
 constexpr int64_t kRowsCap = 1024;           // trace rows per launch
@@ -296,7 +299,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // kLaneVecs vectors are finished by a warp-cooperative scan, 128 entries per
 // step, lowest position winning (ballot + ffs) — the reference's first-hit rule
 // (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
-template <typename OffT, int K>
+template <typename OffT, int K, int LV = kLaneVecs>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const Plane bm,
                                            const bool (&act)[K], const OffT (&s)[K],
                                            const OffT (&e)[K], int64_t (&hit)[K],
@@ -310,7 +313,7 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
         hu[k] = 0;
     }
 #pragma unroll
-    for (int it = 0; it < kLaneVecs; ++it) {
+    for (int it = 0; it < LV; ++it) {
         uint4 q4[K];
         bool go[K];
 #pragma unroll
@@ -731,7 +734,7 @@ struct TileSched {
     }
 };
 
-template <typename OffT, int C>
+template <typename OffT, int C, int LV>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
@@ -794,7 +797,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
             int64_t hit[C];
             uint32_t hu[C];
-            first_hits<OffT, C>(A.adj, in, act, s, e, hit, hu);
+            first_hits<OffT, C, LV>(A.adj, in, act, s, e, hit, hu);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 if (!act[k]) continue;
@@ -888,7 +891,9 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
 
 // K: first-hit searches in flight per lane in the bottom-up phase;
 // MINB: CTAs per SM the register allocation must allow.
-template <typename OffT, int K, int MINB>
+// SCAN: also compile the 4-vector bottom-up path for tiny-frontier layers
+// (large graphs only; it costs registers on the small-graph variant).
+template <typename OffT, int K, int MINB, bool SCAN>
 __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     cg::grid_group grid = cg::this_grid();
     __shared__ TdSmem<OffT> sm;
@@ -960,8 +965,12 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             grid.sync();
             phase_convert(A, A.qb[(L + 1) & 1], out, &ctr->packed, (int32_t)L + 1, true, sm.enq);
         }
-        if (dir == HBFS_BOTTOM_UP)
-            phase_bu<OffT, K>(A, S, in, out, spare, ctr, red, s_found + (threadIdx.x & ~31));
+        if (dir == HBFS_BOTTOM_UP) {
+            uint32_t *sf = s_found + (threadIdx.x & ~31);
+            if (SCAN && S.v_f * 64 < A.n)
+                phase_bu<OffT, K, kLaneVecsScan>(A, S, in, out, spare, ctr, red, sf);
+            else phase_bu<OffT, K, kLaneVecs>(A, S, in, out, spare, ctr, red, sf);
+        }
         grid.sync();
 
         const unsigned long long packed = __ldcg(&ctr->packed);
@@ -1029,11 +1038,11 @@ struct Variant {
 template <typename OffT>
 static const Variant<OffT> *variants(int *count) {
     static const Variant<OffT> v[] = {
-        {(const void *)bfs_kernel<OffT, 2, 1>, 2, 1},
-        {(const void *)bfs_kernel<OffT, 1, 1>, 1, 1},
-        {(const void *)bfs_kernel<OffT, 1, 2>, 1, 2},
-        {(const void *)bfs_kernel<OffT, 2, 2>, 2, 2},
-        {(const void *)bfs_kernel<OffT, 4, 1>, 4, 1},
+        {(const void *)bfs_kernel<OffT, 2, 1, false>, 2, 1},
+        {(const void *)bfs_kernel<OffT, 1, 1, false>, 1, 1},
+        {(const void *)bfs_kernel<OffT, 1, 2, true>, 1, 2},
+        {(const void *)bfs_kernel<OffT, 2, 2, true>, 2, 2},
+        {(const void *)bfs_kernel<OffT, 4, 1, false>, 4, 1},
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
