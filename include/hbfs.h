@@ -134,6 +134,47 @@ int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *level_dev,
                          const int32_t *directions, int64_t n_layers, int64_t *b_sector,
                          int64_t *b_useful, void *stream);
 
+
+/* ---- multi-GPU: one rank's share of a 1D vertex partition ----
+ * Rank r owns vertices [lo, hi) (word aligned) with their CSR rows (global
+ * column ids); frontier and visited bitmaps are replicated, parent/level owned.
+ * The host runs, per layer, hbfs_part_bu or hbfs_part_td_expand + (NCCL
+ * reduce-scatter MIN of the candidates) + hbfs_part_td_finish, then (NCCL
+ * all-gather of the next-frontier slices) + hbfs_part_absorb and an all-reduce
+ * of the counters — paper_1704_02259_b200/mgpu.py.  Replaces, for P > 1, the
+ * same reference interfaces as hbfs_graph_build / hbfs_bfs. */
+typedef struct hbfs_part hbfs_part;
+
+/* Owned rows from the full edge list u,v (every rank passes the same list). */
+int hbfs_part_build(const uint32_t *u, const uint32_t *v, int64_t m, int64_t n, int64_t lo,
+                    int64_t hi, int dedup, int on_device, void *stream, hbfs_part **out);
+/* Owned rows sliced from a reference-layout CSR in host memory. */
+int hbfs_part_from_csr(const int64_t *row_starts, const uint32_t *adjacency, int64_t n,
+                       int64_t lo, int64_t hi, int64_t m_edges, void *stream, hbfs_part **out);
+int hbfs_part_info(const hbfs_part *p, int64_t *n, int64_t *lo, int64_t *hi,
+                   int64_t *local_arcs, int64_t *m_edges);
+/* Degree of v if owned, else 0. */
+int hbfs_part_degree(const hbfs_part *p, int64_t v, int64_t *deg);
+int hbfs_part_free(hbfs_part *p);
+/* Per-root reset: parent/level/frontier/visited with the root. */
+int hbfs_part_init(hbfs_part *p, int64_t root, void *stream);
+/* Bottom-up over owned words against the replicated frontier.  next_slice:
+ * device uint32[ceil((hi-lo)/32)]; counters: device uint64[4] = {found, their
+ * degree sum, gathers, fallbacks} (the reference's 16-lane counters). */
+int hbfs_part_bu(hbfs_part *p, int32_t depth, int32_t max_pos, uint32_t *next_slice,
+                 unsigned long long *counters, void *stream);
+/* Top-down expansion of the owned frontier: cand (device int32[n], pre-filled
+ * with INT32_MAX) receives atomicMin(parent id) for every unvisited target. */
+int hbfs_part_td_expand(hbfs_part *p, int32_t *cand, void *stream);
+/* Apply this rank's MIN-reduced candidate slice (device int32[hi-lo]). */
+int hbfs_part_td_finish(hbfs_part *p, int32_t depth, const int32_t *cand_slice,
+                        uint32_t *next_slice, unsigned long long *counters, void *stream);
+/* next_full: device uint32[ceil(n/32)] all-gathered next frontier. */
+int hbfs_part_absorb(hbfs_part *p, const uint32_t *next_full, void *stream);
+/* Owned parent/level (hi-lo entries each). */
+int hbfs_part_outputs(hbfs_part *p, uint32_t *parent, int32_t *level, int on_device,
+                      void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,18 @@ SIGNATURES = {
     "hbfs_bfs": (C.c_int, [P, i64, C.POINTER(hbfs_params), P, P, C.c_int, P, i64, P, P, P]),
     "hbfs_validate": (C.c_int, [P, i64, P, P, C.c_int, C.c_int, P, P, P]),
     "hbfs_traversal_bytes": (C.c_int, [P, i64, P, P, i64, P, P, P]),
+    # multi-GPU partition (csrc/part.cu)
+    "hbfs_part_build": (C.c_int, [P, P, i64, i64, i64, i64, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "hbfs_part_from_csr": (C.c_int, [P, P, i64, i64, i64, i64, P, C.POINTER(P)]),
+    "hbfs_part_info": (C.c_int, [P, P, P, P, P, P]),
+    "hbfs_part_degree": (C.c_int, [P, i64, P]),
+    "hbfs_part_free": (C.c_int, [P]),
+    "hbfs_part_init": (C.c_int, [P, i64, P]),
+    "hbfs_part_bu": (C.c_int, [P, i32, i32, P, P, P]),
+    "hbfs_part_td_expand": (C.c_int, [P, P, P]),
+    "hbfs_part_td_finish": (C.c_int, [P, i32, P, P, P, P]),
+    "hbfs_part_absorb": (C.c_int, [P, P, P]),
+    "hbfs_part_outputs": (C.c_int, [P, P, P, C.c_int, P]),
 }
 
 _lib = None

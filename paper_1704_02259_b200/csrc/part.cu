@@ -1,0 +1,561 @@
+// Multi-GPU hybrid BFS: one rank's share of a 1D vertex partition.
+//
+// Rank r owns vertices [lo, hi) (word aligned) and holds their CSR rows with
+// global column ids.  The frontier bitmap F and the visited bitmap V are
+// replicated (n bits each); parent/level are owned-only.  Per layer the host
+// (paper_1704_02259_b200/mgpu.py) runs one of
+//   bottom-up:  hbfs_part_bu         -> next-frontier slice of the owned words
+//   top-down:   hbfs_part_td_expand  -> n-sized min-candidate array (int32,
+//                                       INT32_MAX = none) for unvisited targets
+//               [NCCL reduce-scatter(MIN) of the candidates to their owners]
+//               hbfs_part_td_finish  -> owned parents/levels + next slice
+// then [NCCL all-gather of the slices] and hbfs_part_absorb (F = next,
+// V |= next), plus an all-reduce of the four layer counters.  Parents are the
+// global min-id neighbour one level up: bottom-up takes the first
+// frontier hit in the sorted row, top-down the MIN over all ranks' arcs.
+// Replaces, for P > 1, the same reference functions as bfs.cu.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace hbfs {
+
+struct Part {
+    int64_t n = 0, lo = 0, hi = 0, nloc = 0, W = 0, wlo = 0, wloc = 0;
+    int64_t arcs = 0;         // local arcs
+    int64_t m_edges = 0;      // global TEPS denominator
+    DevBuf rs;                // uint64[nloc + 1], local offsets
+    DevBuf adj;               // uint32[arcs + 8], global ids
+    DevBuf F, V;              // uint32[W] replicated
+    DevBuf parent, level;     // owned
+    DevBuf q;                 // uint32[nloc] owned frontier queue
+    DevBuf scratch;           // counters etc.
+};
+
+static inline int pgrid(int64_t items, int block = 256) {
+    int64_t g = (items + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+#define PSTRIDE(i, N) \
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (N); i += (int64_t)gridDim.x * blockDim.x)
+
+// Arcs whose source is owned: key = (local src << sb) | global dst.  key == null
+// only counts (first pass sizes the buffer exactly).
+__global__ void kp_arc_keys(int64_t m, int sb, int64_t lo, int64_t hi, const uint32_t *u,
+                            const uint32_t *v, uint64_t *key, unsigned long long *cnt) {
+    unsigned long long local = 0;
+    PSTRIDE(e, m) {
+        const uint64_t a = u[e], b = v[e];
+        const bool oa = (int64_t)a >= lo && (int64_t)a < hi, ob = (int64_t)b >= lo && (int64_t)b < hi;
+        if (!key) {
+            local += (unsigned long long)oa + (unsigned long long)ob;
+            continue;
+        }
+        if (oa) key[atomicAdd(cnt, 1ull)] = ((a - lo) << sb) | b;
+        if (ob) key[atomicAdd(cnt, 1ull)] = ((b - lo) << sb) | a;
+    }
+    if (!key && local) atomicAdd(cnt, local);
+}
+
+__global__ void kp_dedup_flags(int64_t k, int sb, int64_t lo, const uint64_t *key, uint8_t *keep) {
+    const uint64_t mask = (uint64_t(1) << sb) - 1;
+    PSTRIDE(i, k) {
+        const uint64_t x = key[i];
+        const bool self = (int64_t)((x >> sb) + lo) == (int64_t)(x & mask);
+        keep[i] = !(self || (i > 0 && key[i - 1] == x));
+    }
+}
+
+__global__ void kp_adj(int64_t k, int sb, const uint64_t *key, uint32_t *adj) {
+    const uint64_t mask = (uint64_t(1) << sb) - 1;
+    PSTRIDE(i, k) adj[i] = (uint32_t)(key[i] & mask);
+}
+
+__global__ void kp_rs(int64_t nloc, int64_t k, int sb, const uint64_t *key, uint64_t *rs) {
+    PSTRIDE(v, nloc + 1) {
+        const uint64_t target = (uint64_t)v << sb;
+        int64_t lo = 0, hi = k;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (key[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        rs[v] = (uint64_t)lo;
+    }
+}
+
+__global__ void kp_slice_rs(int64_t nloc, const int64_t *grs, int64_t lo, uint64_t *rs) {
+    PSTRIDE(v, nloc + 1) rs[v] = (uint64_t)(grs[lo + v] - grs[lo]);
+}
+
+__global__ void kp_init(int64_t nloc, int64_t W, int64_t lo, uint32_t root, uint32_t *parent,
+                        int32_t *level, uint32_t *F, uint32_t *V) {
+    PSTRIDE(i, nloc) {
+        const bool r = lo + i == (int64_t)root;
+        parent[i] = r ? root : HBFS_NIL;
+        level[i] = r ? 0 : -1;
+    }
+    PSTRIDE(w, W) {
+        const uint32_t b = (w == (int64_t)(root >> 5)) ? (1u << (root & 31)) : 0u;
+        F[w] = b;
+        V[w] = b;
+    }
+}
+
+// Bottom-up over the owned words: warp per word, lane per vertex, row probes in
+// ascending position with warp-cooperative tails (first hit = min position).
+__global__ void kp_bu(int64_t wloc, int64_t nloc, int64_t lo, int32_t depth1, int64_t max_pos,
+                      const uint64_t *rs, const uint32_t *adj, const uint32_t *F, uint32_t *V,
+                      uint32_t *parent, int32_t *level, uint32_t *next,
+                      unsigned long long *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wlo = lo >> 5;
+    unsigned long long c_cnt = 0, c_deg = 0, c_gat = 0, c_fb = 0;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < wloc;
+         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t vw = V[wlo + j];
+        const int64_t lv = j * 32 + lane;  // local vertex
+        const bool valid = lv < nloc;
+        const uint64_t s = valid ? rs[lv] : 0, e = valid ? rs[lv + 1] : 0;
+        const bool mine = valid && !((vw >> lane) & 1u) && e > s;
+        int64_t hit = -1;
+        uint32_t hu = 0;
+        uint64_t p = s;
+        if (mine) {
+            for (int it = 0; it < 8 && p < e; ++it, ++p) {
+                const uint32_t a = adj[p];
+                if ((F[a >> 5] >> (a & 31)) & 1u) {
+                    hit = (int64_t)p;
+                    hu = a;
+                    break;
+                }
+            }
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, mine && hit < 0 && p < e);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint64_t ps = __shfl_sync(0xffffffffu, p, src), pe = __shfl_sync(0xffffffffu, e, src);
+            int64_t h = -1;
+            uint32_t hv = 0;
+            for (uint64_t c = ps; c < pe; c += 32) {
+                const uint64_t k = c + lane;
+                uint32_t a = 0;
+                const bool bit = k < pe && ((F[(a = adj[k]) >> 5] >> (a & 31)) & 1u);
+                const unsigned b = __ballot_sync(0xffffffffu, bit);
+                if (b) {
+                    const int l = __ffs(b) - 1;
+                    h = (int64_t)(c + l);
+                    hv = __shfl_sync(0xffffffffu, a, l);
+                    break;
+                }
+            }
+            if (lane == src) {
+                hit = h;
+                hu = hv;
+            }
+        }
+        const bool found = hit >= 0;
+        if (found) {
+            parent[lv] = hu;
+            level[lv] = depth1;
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, found);
+        if (lane == 0) next[j] = fm;
+        if (mine) {
+            const int64_t deg = (int64_t)(e - s);
+            const int64_t pos = found ? hit - (int64_t)s : -1;
+            const bool early = found && pos < max_pos;
+            if (found) {
+                c_cnt += 1;
+                c_deg += (unsigned long long)deg;
+            }
+            c_gat += early ? (unsigned long long)(pos + 1) : (unsigned long long)(deg < max_pos ? deg : max_pos);
+            c_fb += (deg > max_pos && !early) ? 1ull : 0ull;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c_cnt += __shfl_down_sync(0xffffffffu, c_cnt, o);
+        c_deg += __shfl_down_sync(0xffffffffu, c_deg, o);
+        c_gat += __shfl_down_sync(0xffffffffu, c_gat, o);
+        c_fb += __shfl_down_sync(0xffffffffu, c_fb, o);
+    }
+    if (lane == 0) {
+        if (c_cnt) atomicAdd(&ctr[0], c_cnt);
+        if (c_deg) atomicAdd(&ctr[1], c_deg);
+        if (c_gat) atomicAdd(&ctr[2], c_gat);
+        if (c_fb) atomicAdd(&ctr[3], c_fb);
+    }
+}
+
+// owned frontier queue from the replicated F
+__global__ void kp_queue(int64_t wloc, int64_t lo, const uint32_t *F, uint32_t *q,
+                         unsigned long long *qn) {
+    PSTRIDE(j, wloc) {
+        uint32_t bits = F[(lo >> 5) + j];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            q[atomicAdd(qn, 1ull)] = (uint32_t)(j * 32 + b);  // local id
+        }
+    }
+}
+
+// Top-down expansion: warp per frontier row for short rows, the whole CTA for
+// rows of >= 1024 arcs; every arc into an unvisited target lowers cand[v].
+__global__ void kp_td(const uint32_t *q, int64_t qn, int64_t lo, const uint64_t *rs,
+                      const uint32_t *adj, const uint32_t *V, int32_t *cand, int big) {
+    const int lane = threadIdx.x & 31;
+    if (!big) {
+        for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
+             i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+            const uint32_t ul = q[i];
+            const uint64_t s = rs[ul], e = rs[ul + 1];
+            if (e - s >= 1024) continue;
+            const int32_t u = (int32_t)(lo + ul);
+            for (uint64_t k = s + lane; k < e; k += 32) {
+                const uint32_t v = adj[k];
+                if (!((V[v >> 5] >> (v & 31)) & 1u)) atomicMin(&cand[v], u);
+            }
+        }
+    } else {
+        for (int64_t i = blockIdx.x; i < qn; i += gridDim.x) {
+            const uint32_t ul = q[i];
+            const uint64_t s = rs[ul], e = rs[ul + 1];
+            if (e - s < 1024) continue;
+            const int32_t u = (int32_t)(lo + ul);
+            for (uint64_t k = s + threadIdx.x; k < e; k += blockDim.x) {
+                const uint32_t v = adj[k];
+                if (!((V[v >> 5] >> (v & 31)) & 1u)) atomicMin(&cand[v], u);
+            }
+        }
+    }
+}
+
+// Owned slice of the MIN-reduced candidates -> parents, levels, next slice.
+__global__ void kp_td_finish(int64_t wloc, int64_t nloc, int32_t depth1, const int32_t *cand,
+                             const uint64_t *rs,
+                             uint32_t *parent, int32_t *level, uint32_t *next,
+                             unsigned long long *ctr) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long c_cnt = 0, c_deg = 0;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < wloc;
+         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t lv = j * 32 + lane;
+        const int32_t c = lv < nloc ? cand[lv] : 0x7FFFFFFF;
+        const bool found = c != 0x7FFFFFFF;
+        if (found) {
+            parent[lv] = (uint32_t)c;
+            level[lv] = depth1;
+            c_cnt += 1;
+            c_deg += (unsigned long long)(rs[lv + 1] - rs[lv]);
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, found);
+        if (lane == 0) next[j] = fm;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c_cnt += __shfl_down_sync(0xffffffffu, c_cnt, o);
+        c_deg += __shfl_down_sync(0xffffffffu, c_deg, o);
+    }
+    if (lane == 0) {
+        if (c_cnt) atomicAdd(&ctr[0], c_cnt);
+        if (c_deg) atomicAdd(&ctr[1], c_deg);
+    }
+}
+
+__global__ void kp_absorb(int64_t W, const uint32_t *next, uint32_t *F, uint32_t *V) {
+    PSTRIDE(w, W) {
+        const uint32_t x = next[w];
+        F[w] = x;
+        if (x) V[w] |= x;
+    }
+}
+
+static int part_alloc_state(Part *P) {
+    HB_CHECK(P->F.alloc(P->W * 4 + 16));
+    HB_CHECK(P->V.alloc(P->W * 4 + 16));
+    HB_CHECK(P->parent.alloc(P->nloc * 4 + 16));
+    HB_CHECK(P->level.alloc(P->nloc * 4 + 16));
+    HB_CHECK(P->q.alloc(P->nloc * 4 + 16));
+    HB_CHECK(P->scratch.alloc(64));
+    return HBFS_OK;
+}
+
+static int check_range(int64_t n, int64_t lo, int64_t hi) {
+    if (lo < 0 || hi > n || lo >= hi || (lo & 31) || ((hi & 31) && hi != n))
+        return set_error(HBFS_EINVAL, "owned range must be word aligned inside [0, n)");
+    return HBFS_OK;
+}
+
+}  // namespace hbfs
+
+using namespace hbfs;
+
+struct hbfs_part : Part {};
+
+extern "C" int hbfs_part_build(const uint32_t *u, const uint32_t *v, int64_t m, int64_t n,
+                               int64_t lo, int64_t hi, int dedup, int on_device, void *stream,
+                               hbfs_part **out) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!out || m < 0 || n <= 0) return set_error(HBFS_EINVAL, "bad arguments");
+    HB_CHECK(check_range(n, lo, hi));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DevBuf du, dv, k0, k1, tmp, cnt;
+    const uint32_t *pu = u, *pv = v;
+    if (!on_device) {
+        HB_CHECK(du.alloc(m * 4 + 16));
+        HB_CHECK(dv.alloc(m * 4 + 16));
+        HB_CUDA(cudaMemcpyAsync(du.p, u, m * 4, cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemcpyAsync(dv.p, v, m * 4, cudaMemcpyHostToDevice, st));
+        pu = du.as<uint32_t>();
+        pv = dv.as<uint32_t>();
+    }
+    int sb = 1;
+    while ((int64_t(1) << sb) < n) ++sb;
+    HB_CHECK(cnt.alloc(8));
+    HB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+    // count first so the key buffer is sized exactly, then fill
+    kp_arc_keys<<<pgrid(m), 256, 0, st>>>(m, sb, lo, hi, pu, pv, nullptr, cnt.as<unsigned long long>());
+    HB_CUDA(cudaGetLastError());
+    unsigned long long kk = 0;
+    HB_CUDA(cudaMemcpyAsync(&kk, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    int64_t k = (int64_t)kk;
+    HB_CHECK(k0.alloc(k * 8 + 16));
+    HB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+    kp_arc_keys<<<pgrid(m), 256, 0, st>>>(m, sb, lo, hi, pu, pv, k0.as<uint64_t>(),
+                                          cnt.as<unsigned long long>());
+    HB_CUDA(cudaGetLastError());
+    hbfs_part *P = new hbfs_part();
+    P->n = n;
+    P->lo = lo;
+    P->hi = hi;
+    P->nloc = hi - lo;
+    P->W = (n + 31) / 32;
+    P->wlo = lo >> 5;
+    P->wloc = (P->nloc + 31) / 32;
+    P->m_edges = m;
+    int rc = HBFS_OK;
+    if (!rc) rc = k1.alloc(k * 8 + 16);
+    const int key_bits = 2 * sb;
+    if (!rc && k > 0) {
+        cub::DoubleBuffer<uint64_t> db(k0.as<uint64_t>(), k1.as<uint64_t>());
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, db, k, 0, key_bits, st);
+        rc = tmp.alloc(tb);
+        if (!rc && cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, k, 0, key_bits, st) != cudaSuccess)
+            rc = set_error(HBFS_ECUDA, "sort failed");
+        uint64_t *sorted = db.Current();
+        if (!rc && dedup) {
+            DevBuf flags, nsel, tmp2;
+            rc = flags.alloc(k);
+            if (!rc) rc = nsel.alloc(8);
+            if (!rc) {
+                kp_dedup_flags<<<pgrid(k), 256, 0, st>>>(k, sb, lo, sorted, flags.as<uint8_t>());
+                size_t tb2 = 0;
+                cub::DeviceSelect::Flagged(nullptr, tb2, sorted, flags.as<uint8_t>(), db.Alternate(),
+                                           nsel.as<int64_t>(), k, st);
+                rc = tmp2.alloc(tb2);
+                if (!rc) cub::DeviceSelect::Flagged(tmp2.p, tb2, sorted, flags.as<uint8_t>(),
+                                                    db.Alternate(), nsel.as<int64_t>(), k, st);
+                int64_t h = 0;
+                cudaMemcpyAsync(&h, nsel.p, 8, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                k = h;
+                sorted = db.Alternate();
+            }
+        }
+        if (!rc) rc = P->adj.alloc((k + 8) * 4);
+        if (!rc) rc = P->rs.alloc((P->nloc + 1) * 8);
+        if (!rc) {
+            kp_adj<<<pgrid(k), 256, 0, st>>>(k, sb, sorted, P->adj.as<uint32_t>());
+            kp_rs<<<pgrid(P->nloc + 1), 256, 0, st>>>(P->nloc, k, sb, sorted, P->rs.as<uint64_t>());
+            if (cudaGetLastError() != cudaSuccess) rc = set_error(HBFS_ECUDA, "csr kernels failed");
+        }
+    } else if (!rc) {
+        rc = P->adj.alloc(64);
+        if (!rc) rc = P->rs.alloc((P->nloc + 1) * 8);
+        if (!rc) cudaMemsetAsync(P->rs.p, 0, (P->nloc + 1) * 8, st);
+    }
+    P->arcs = k;
+    if (!rc) rc = part_alloc_state(P);
+    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = set_error(HBFS_ECUDA, "build failed");
+    if (rc) {
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_part_from_csr(const int64_t *row_starts, const uint32_t *adjacency, int64_t n,
+                                  int64_t lo, int64_t hi, int64_t m_edges, void *stream,
+                                  hbfs_part **out) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!out || !row_starts || n <= 0) return set_error(HBFS_EINVAL, "bad arguments");
+    HB_CHECK(check_range(n, lo, hi));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    hbfs_part *P = new hbfs_part();
+    P->n = n;
+    P->lo = lo;
+    P->hi = hi;
+    P->nloc = hi - lo;
+    P->W = (n + 31) / 32;
+    P->wlo = lo >> 5;
+    P->wloc = (P->nloc + 31) / 32;
+    P->m_edges = m_edges;
+    const int64_t a0 = row_starts[lo], a1 = row_starts[hi];
+    P->arcs = a1 - a0;
+    DevBuf grs;
+    int rc = grs.alloc((P->nloc + 1) * 8);
+    if (!rc) rc = P->rs.alloc((P->nloc + 1) * 8);
+    if (!rc) rc = P->adj.alloc((P->arcs + 8) * 4);
+    if (!rc && cudaMemcpyAsync(grs.p, row_starts + lo, (P->nloc + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = set_error(HBFS_ECUDA, "copy failed");
+    if (!rc && P->arcs > 0 &&
+        cudaMemcpyAsync(P->adj.p, adjacency + a0, P->arcs * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = set_error(HBFS_ECUDA, "copy failed");
+    if (!rc) {
+        kp_slice_rs<<<pgrid(P->nloc + 1), 256, 0, st>>>(P->nloc, grs.as<int64_t>(), 0, P->rs.as<uint64_t>());
+        if (cudaGetLastError() != cudaSuccess) rc = set_error(HBFS_ECUDA, "slice failed");
+    }
+    if (!rc) rc = part_alloc_state(P);
+    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = set_error(HBFS_ECUDA, "import failed");
+    if (rc) {
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_part_info(const hbfs_part *P, int64_t *n, int64_t *lo, int64_t *hi,
+                              int64_t *local_arcs, int64_t *m_edges) {
+    if (!P) return set_error(HBFS_EINVAL, "null part");
+    if (n) *n = P->n;
+    if (lo) *lo = P->lo;
+    if (hi) *hi = P->hi;
+    if (local_arcs) *local_arcs = P->arcs;
+    if (m_edges) *m_edges = P->m_edges;
+    return HBFS_OK;
+}
+
+extern "C" int hbfs_part_free(hbfs_part *P) {
+    HB_ENTRY_BEGIN
+    delete P;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_part_degree(const hbfs_part *P, int64_t v, int64_t *deg) {
+    HB_ENTRY_BEGIN
+    if (!P || !deg) return set_error(HBFS_EINVAL, "bad arguments");
+    *deg = 0;
+    if (v < P->lo || v >= P->hi) return HBFS_OK;
+    uint64_t h[2];
+    HB_CUDA(cudaMemcpy(h, P->rs.as<uint64_t>() + (v - P->lo), 16, cudaMemcpyDeviceToHost));
+    *deg = (int64_t)(h[1] - h[0]);
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_part_init(hbfs_part *P, int64_t root, void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P) return set_error(HBFS_EINVAL, "null part");
+    if (root < 0 || root >= P->n) return set_error(HBFS_ERANGE, "source out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    kp_init<<<pgrid(std::max(P->nloc, P->W)), 256, 0, st>>>(
+        P->nloc, P->W, P->lo, (uint32_t)root, P->parent.as<uint32_t>(), P->level.as<int32_t>(),
+        P->F.as<uint32_t>(), P->V.as<uint32_t>());
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// counters: device uint64[4] = {found, degree sum of found, gathers, fallbacks}
+extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32_t *next_slice,
+                            unsigned long long *counters, void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    HB_CUDA(cudaMemsetAsync(counters, 0, 32, st));
+    kp_bu<<<pgrid(P->wloc * 32), 256, 0, st>>>(P->wloc, P->nloc, P->lo, depth + 1, max_pos,
+                                               P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
+                                               P->F.as<uint32_t>(), P->V.as<uint32_t>(),
+                                               P->parent.as<uint32_t>(), P->level.as<int32_t>(),
+                                               next_slice, counters);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// cand: device int32[n], pre-filled with INT32_MAX by the caller
+extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t *cand, void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P || !cand) return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long *qn = P->scratch.as<unsigned long long>();
+    HB_CUDA(cudaMemsetAsync(qn, 0, 8, st));
+    kp_queue<<<pgrid(P->wloc), 256, 0, st>>>(P->wloc, P->lo, P->F.as<uint32_t>(),
+                                             P->q.as<uint32_t>(), qn);
+    HB_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    HB_CUDA(cudaMemcpyAsync(&h, qn, 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (h > 0) {
+        kp_td<<<pgrid((int64_t)h * 32), 256, 0, st>>>(P->q.as<uint32_t>(), (int64_t)h, P->lo,
+                                                      P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
+                                                      P->V.as<uint32_t>(), cand, 0);
+        kp_td<<<(int)std::min<int64_t>((int64_t)h, 148 * 8), 512, 0, st>>>(
+            P->q.as<uint32_t>(), (int64_t)h, P->lo, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
+            P->V.as<uint32_t>(), cand, 1);
+        HB_CUDA(cudaGetLastError());
+    }
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// cand_slice: device int32[nloc] (this rank's MIN-reduced candidates)
+extern "C" int hbfs_part_td_finish(hbfs_part *P, int32_t depth, const int32_t *cand_slice,
+                                   uint32_t *next_slice, unsigned long long *counters,
+                                   void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P || !cand_slice || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    HB_CUDA(cudaMemsetAsync(counters, 0, 32, st));
+    kp_td_finish<<<pgrid(P->wloc * 32), 256, 0, st>>>(P->wloc, P->nloc, depth + 1, cand_slice,
+                                                      P->rs.as<uint64_t>(), P->parent.as<uint32_t>(),
+                                                      P->level.as<int32_t>(), next_slice, counters);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// next_full: device uint32[W] (all-gathered next frontier): F = next, V |= next
+extern "C" int hbfs_part_absorb(hbfs_part *P, const uint32_t *next_full, void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P || !next_full) return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    kp_absorb<<<pgrid(P->W), 256, 0, st>>>(P->W, next_full, P->F.as<uint32_t>(), P->V.as<uint32_t>());
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_part_outputs(hbfs_part *P, uint32_t *parent, int32_t *level, int on_device,
+                                 void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P) return set_error(HBFS_EINVAL, "null part");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (parent) HB_CUDA(cudaMemcpyAsync(parent, P->parent.p, P->nloc * 4, k, st));
+    if (level) HB_CUDA(cudaMemcpyAsync(level, P->level.p, P->nloc * 4, k, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    return HBFS_OK;
+    HB_ENTRY_END
+}

@@ -1,0 +1,370 @@
+"""Multi-GPU hybrid BFS: 1D vertex partition over P ranks.
+
+Rank r owns a contiguous, word-aligned block of vertices with their CSR rows
+(global column ids).  The frontier and visited bitmaps are replicated; parent
+and level are owned.  Per layer (the controller is the reference's,
+hybrid.py:83-175, with the same trace):
+
+* bottom-up: local bottom-up over the owned words against the replicated
+  frontier (parents need no communication: rows are local);
+* top-down: local expansion of the owned frontier into an n-sized min-candidate
+  array, **reduce-scatter(MIN)** to the owners (exact min-id parents);
+* then **all-gather** of the next-frontier slices (the new replicated frontier,
+  also OR-ed into the replicated visited bitmap) and an **all-reduce(SUM)** of
+  the four layer counters, so every rank takes the same direction decision.
+
+The per-rank compute is a ``RankOps`` object: ``CudaRankOps`` runs the sm_100a
+kernels of ``csrc/part.cu`` (the product); tests also plug in the CPU rank of
+``oracle/part_cpu.py`` to cover this host logic with gloo on CPU.  The
+communicator is either ``TorchComm`` (one rank per process, torch.distributed
+with NCCL on GPUs / gloo on CPU) or ``LocalComm`` (P logical ranks driven by one
+process — used to test the partitioned CUDA path on a single GPU; it never runs
+kernels that wait on one another).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .hybrid import BOTTOM_UP, TOP_DOWN, HEURISTICS, COUNTER_MODES, HeuristicParams, LayerTraceRow
+from .lanes import VecConfig
+
+INT32_MAX = 0x7FFFFFFF
+
+
+def partition(n: int, world: int, rank: int):
+    """Owned vertex range [lo, hi) of `rank`: equal word counts per rank."""
+    W = (n + 31) // 32
+    wper = (W + world - 1) // world
+    lo = min(rank * wper * 32, n)
+    hi = min((rank + 1) * wper * 32, n)
+    return lo, hi, wper
+
+
+def decide(p: HeuristicParams, cur: int, v_f: int, e_f: int, eu_v: int, eu_e: int, prev_vf: int,
+           n: int, force: int):
+    """Host restatement of csrc/bfs.cu ``decide`` (reference rule hybrid.py:72-80,
+    or Beamer/GAP).  Returns (direction 0/1, f_value, g_value)."""
+    gv = n // p.beta
+    if p.heuristic == "beamer":
+        fv = eu_e // p.alpha
+        if force >= 0:
+            return force, fv, gv
+        if cur == 0:
+            return (1 if e_f > fv else 0), fv, gv
+        return (0 if (v_f < prev_vf and v_f <= gv) else 1), fv, gv
+    e_u = eu_e if p.counter_mode == "edge" else eu_v
+    fv = e_u // p.alpha
+    if force >= 0:
+        return force, fv, gv
+    if v_f > fv:
+        return 1, fv, gv
+    if v_f < gv:
+        return 0, fv, gv
+    return cur, fv, gv
+
+
+# ------------------------------------------------------------ communicators
+
+class TorchComm:
+    """One rank per process; collectives through torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.backend = dist.get_backend(group)
+        self.local_ranks = [self.rank]
+
+    def all_gather(self, slices):
+        import torch
+
+        s = slices[0]
+        out = torch.empty(s.numel() * self.world, dtype=s.dtype, device=s.device)
+        if self.backend == "nccl":
+            self.dist.all_gather_into_tensor(out, s, group=self.group)
+        else:
+            self.dist.all_gather(list(out.chunk(self.world)), s, group=self.group)
+        return [out]
+
+    def reduce_scatter_min(self, fulls):
+        full = fulls[0]
+        chunk = full.numel() // self.world
+        if self.backend == "nccl":
+            import torch
+
+            out = torch.empty(chunk, dtype=full.dtype, device=full.device)
+            self.dist.reduce_scatter_tensor(out, full, op=self.dist.ReduceOp.MIN, group=self.group)
+            return [out]
+        # gloo has no reduce_scatter: all-reduce then keep the owned chunk
+        self.dist.all_reduce(full, op=self.dist.ReduceOp.MIN, group=self.group)
+        return [full[self.rank * chunk:(self.rank + 1) * chunk].clone()]
+
+    def all_reduce_sum(self, tensors):
+        self.dist.all_reduce(tensors[0], op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def all_reduce_max_float(self, x: float) -> float:
+        import torch
+
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class LocalComm:
+    """P logical ranks in one process (one GPU): collectives are tensor ops."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.rank = 0
+        self.local_ranks = list(range(world))
+
+    def all_gather(self, slices):
+        import torch
+
+        full = torch.cat(list(slices))
+        return [full.clone() for _ in slices]
+
+    def reduce_scatter_min(self, fulls):
+        import torch
+
+        m = fulls[0].clone()
+        for f in fulls[1:]:
+            m = torch.minimum(m, f)
+        return [c.clone() for c in m.chunk(self.world)]
+
+    def all_reduce_sum(self, tensors):
+        tot = tensors[0].clone()
+        for t in tensors[1:]:
+            tot += t
+        for t in tensors:
+            t.copy_(tot)
+
+    def all_reduce_max_float(self, x: float) -> float:
+        return x
+
+    def barrier(self):
+        pass
+
+
+# -------------------------------------------------------------- CUDA rank
+
+class CudaRankOps:
+    """One rank's partition on the current CUDA device (csrc/part.cu)."""
+
+    def __init__(self, handle, device):
+        from . import _lib
+
+        self._lib = _lib
+        self.lib = _lib.load(require_device=True)
+        self.h = handle
+        self.device = device
+        n, lo, hi, la, m = (C.c_int64() for _ in range(5))
+        _lib.check(self.lib.hbfs_part_info(handle, C.byref(n), C.byref(lo), C.byref(hi),
+                                           C.byref(la), C.byref(m)))
+        self.n, self.lo, self.hi = n.value, lo.value, hi.value
+        self.local_arcs, self.m_edges = la.value, m.value
+        self.nloc = self.hi - self.lo
+
+    @classmethod
+    def generate(cls, params, world: int, rank: int, dedup: bool = False, device=None):
+        """Every rank generates the full edge list on its GPU (bit-exact device
+        generator) and keeps the rows it owns."""
+        import torch
+
+        from . import _lib
+        from .generator import thresholds
+
+        lib = _lib.load(require_device=True)
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        n, m = params.num_vertices, params.num_edges
+        lo, hi, _ = partition(n, world, rank)
+        u = torch.empty(m, dtype=torch.int32, device=dev)
+        v = torch.empty(m, dtype=torch.int32, device=dev)
+        thr = thresholds(params.probs)
+        _lib.check(lib.hbfs_generate_edges(params.scale, params.edgefactor,
+                                           params.seed & 0xFFFFFFFFFFFFFFFF,
+                                           thr.ctypes.data_as(C.c_void_p), int(params.permute_labels),
+                                           C.c_void_p(u.data_ptr()), C.c_void_p(v.data_ptr()), 1, None))
+        h = C.c_void_p()
+        _lib.check(lib.hbfs_part_build(C.c_void_p(u.data_ptr()), C.c_void_p(v.data_ptr()), m, n, lo,
+                                       hi, int(dedup), 1, None, C.byref(h)))
+        del u, v
+        return cls(h, dev)
+
+    @classmethod
+    def from_csr(cls, row_starts, adjacency, m_edges: int, world: int, rank: int, device=None):
+        import torch
+
+        from . import _lib
+
+        lib = _lib.load(require_device=True)
+        rs = np.ascontiguousarray(row_starts, dtype=np.int64)
+        adj = np.ascontiguousarray(adjacency, dtype=np.uint32)
+        n = len(rs) - 1
+        lo, hi, _ = partition(n, world, rank)
+        h = C.c_void_p()
+        _lib.check(lib.hbfs_part_from_csr(rs.ctypes.data_as(C.c_void_p), adj.ctypes.data_as(C.c_void_p),
+                                          n, lo, hi, m_edges, None, C.byref(h)))
+        return cls(h, device or torch.device("cuda", torch.cuda.current_device()))
+
+    def free(self):
+        if self.h is not None:
+            self.lib.hbfs_part_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def _s(self):
+        return self._lib.current_stream()
+
+    def degree(self, v: int) -> int:
+        d = C.c_int64()
+        self._lib.check(self.lib.hbfs_part_degree(self.h, v, C.byref(d)))
+        return d.value
+
+    def init(self, root: int):
+        self._lib.check(self.lib.hbfs_part_init(self.h, root, self._s()))
+
+    def bu(self, depth, max_pos, next_slice, ctr):
+        self._lib.check(self.lib.hbfs_part_bu(self.h, depth, max_pos, C.c_void_p(next_slice.data_ptr()),
+                                              C.c_void_p(ctr.data_ptr()), self._s()))
+
+    def td_expand(self, cand):
+        self._lib.check(self.lib.hbfs_part_td_expand(self.h, C.c_void_p(cand.data_ptr()), self._s()))
+
+    def td_finish(self, depth, cand_slice, next_slice, ctr):
+        self._lib.check(self.lib.hbfs_part_td_finish(self.h, depth, C.c_void_p(cand_slice.data_ptr()),
+                                                     C.c_void_p(next_slice.data_ptr()),
+                                                     C.c_void_p(ctr.data_ptr()), self._s()))
+
+    def absorb(self, next_full):
+        self._lib.check(self.lib.hbfs_part_absorb(self.h, C.c_void_p(next_full.data_ptr()), self._s()))
+
+    def outputs(self):
+        par = np.empty(self.nloc, dtype=np.uint32)
+        lev = np.empty(self.nloc, dtype=np.int32)
+        self._lib.check(self.lib.hbfs_part_outputs(self.h, par.ctypes.data_as(C.c_void_p),
+                                                   lev.ctypes.data_as(C.c_void_p), 0, self._s()))
+        return par, lev
+
+    def new_tensor(self, size, dtype_name):
+        import torch
+
+        return torch.empty(size, dtype=getattr(torch, dtype_name), device=self.device)
+
+
+# ------------------------------------------------------------- controller
+
+@dataclass
+class DistResult:
+    trace: list
+    seconds: float
+
+
+class DistBfs:
+    """Drives the per-layer steps of every rank this process owns (one for
+    TorchComm, P for LocalComm) with the same host decisions on all ranks."""
+
+    def __init__(self, ranks, comm):
+        self.ranks = list(ranks)
+        self.comm = comm
+        r0 = self.ranks[0]
+        self.n = r0.n
+        self.world = comm.world
+        _, _, self.wper = partition(self.n, self.world, 0)
+        self.W = (self.n + 31) // 32
+        arcs = [self._i64([r.local_arcs]) for r in self.ranks]
+        comm.all_reduce_sum(arcs)
+        self.arcs_global = int(arcs[0][0].item())
+        self.m_edges = r0.m_edges
+
+    def _i64(self, vals):
+        r0 = self.ranks[0]
+        t = r0.new_tensor(len(vals), "int64")
+        t.copy_(self._torch().tensor(vals, dtype=self._torch().int64))
+        return t
+
+    @staticmethod
+    def _torch():
+        import torch
+
+        return torch
+
+    def bfs(self, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = None,
+            use_simd: bool = True, force_direction=None) -> DistResult:
+        torch = self._torch()
+        p = p if p is not None else HeuristicParams()
+        cfg = cfg if cfg is not None else VecConfig()
+        if not 0 <= root < self.n:
+            raise IndexError(f"source {root} out of range [0, {self.n})")
+        force = {None: -1, TOP_DOWN: 0, BOTTOM_UP: 1}[force_direction]
+        R = self.ranks
+        t0 = time.perf_counter()
+        for r in R:
+            r.init(root)
+        degs = [self._i64([r.degree(root)]) for r in R]
+        self.comm.all_reduce_sum(degs)
+        rdeg = int(degs[0][0].item())
+        v_f, e_f, eu_v, eu_e, prev_vf, cur = 1, rdeg, self.n - 1, self.arcs_global - rdeg, 0, 0
+        slices = [r.new_tensor(self.wper, "int32") for r in R]
+        ctrs = [r.new_tensor(4, "int64") for r in R]
+        cands = None
+        trace = []
+        layer = 0
+        while v_f > 0:
+            d, fv, gv = decide(p, cur, v_f, e_f, eu_v, eu_e, prev_vf, self.n, force)
+            for s in slices:
+                s.zero_()
+            tl = time.perf_counter()
+            if d == 1:
+                for r, s, c in zip(R, slices, ctrs):
+                    r.bu(layer, cfg.max_pos, s, c)
+            else:
+                if cands is None:
+                    cands = [r.new_tensor(self.world * self.wper * 32, "int32") for r in R]
+                for r, cd in zip(R, cands):
+                    cd.fill_(INT32_MAX)
+                    r.td_expand(cd)
+                owned = self.comm.reduce_scatter_min(cands)
+                for r, o, s, c in zip(R, owned, slices, ctrs):
+                    r.td_finish(layer, o, s, c)
+            fulls = self.comm.all_gather(slices)
+            self.comm.all_reduce_sum(ctrs)
+            for r, f in zip(R, fulls):
+                r.absorb(f)
+            nvf, nef, gat, fb = (int(x) for x in ctrs[0].tolist())
+            if d == 0:
+                gat, fb = e_f, 0
+            if not use_simd:
+                gat, fb = 0, 0
+            trace.append(LayerTraceRow(
+                layer=layer + 1, direction=BOTTOM_UP if d else TOP_DOWN,
+                kernel="simd" if use_simd else "scalar", v_f=v_f, e_f=e_f,
+                e_u=eu_e if p.counter_mode == "edge" else eu_v, f_value=fv, g_value=gv,
+                elapsed=time.perf_counter() - tl, fallback_count=fb, gather_count=gat))
+            prev_vf, v_f, e_f = v_f, nvf, nef
+            eu_v -= nvf
+            eu_e -= nef
+            cur = d
+            layer += 1
+        return DistResult(trace=trace, seconds=time.perf_counter() - t0)
+
+    def outputs(self):
+        """Owned (parent, level) of each local rank, in rank order."""
+        return [r.outputs() for r in self.ranks]
