@@ -1,0 +1,67 @@
+"""Partitioned (multi-GPU) CUDA kernels on one GPU: P logical ranks driven by one
+process through mgpu.LocalComm (collectives as tensor ops; no kernel waits on
+another).  Levels, min-id parents and traces must equal the reference's."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MODES = {
+    "simd_default": dict(use_simd=True),
+    "simd_a14b24": dict(use_simd=True, p=dict(alpha=14, beta=24)),
+    "simd_edge": dict(use_simd=True, p=dict(counter_mode="edge")),
+    "force_td": dict(use_simd=False, force_direction="top-down"),
+    "force_bu": dict(use_simd=True, force_direction="bottom-up"),
+}
+
+
+def trace_array(trace):
+    return np.array([[r.layer, 1 if r.direction == "bottom-up" else 0, r.v_f, r.e_f, r.e_u,
+                      r.f_value, r.g_value, r.fallback_count, r.gather_count] for r in trace],
+                    dtype=np.int64).reshape(-1, 9)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("name", ["k8", "k10", "u12"])
+def test_partitioned_cuda_ranks(cuda, small_golden, golden_hashes, world, name):
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm
+
+    rs, adj = small_golden[f"{name}/rs"], small_golden[f"{name}/adj"]
+    m = len(adj) // 2
+    ranks = [CudaRankOps.from_csr(rs, adj, m, world, r) for r in range(world)]
+    db = DistBfs(ranks, LocalComm(world))
+    for s in small_golden[f"{name}/sources"][:4]:
+        s = int(s)
+        for mode, kw in MODES.items():
+            p = hb.HeuristicParams(**kw.get("p", {}))
+            res = db.bfs(s, p, use_simd=kw["use_simd"], force_direction=kw.get("force_direction"))
+            outs = db.outputs()
+            par = np.concatenate([o[0] for o in outs])
+            lev = np.concatenate([o[1] for o in outs])
+            assert np.array_equal(lev, small_golden[f"{name}/{s}/level"]), (name, world, s, mode)
+            assert np.array_equal(par, small_golden[f"{name}/{s}/{mode}/parent"]), (name, world, s, mode)
+            assert np.array_equal(trace_array(res.trace), small_golden[f"{name}/{s}/{mode}/trace"]), (name, world, s, mode)
+
+
+def test_partitioned_generate_matches_single_gpu(cuda):
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm
+
+    params = hb.GraphParams(scale=14, edgefactor=16, seed=1)
+    g = hb.generate_graph(params)
+    roots = hb.sample_sources(g, 6, 1)
+    for world in (2, 4):
+        ranks = [CudaRankOps.generate(params, world, r) for r in range(world)]
+        db = DistBfs(ranks, LocalComm(world))
+        p = hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge")
+        for s in roots:
+            ref = hb.bfs(g, int(s), p, device=False)
+            res = db.bfs(int(s), p)
+            outs = db.outputs()
+            assert np.array_equal(np.concatenate([o[1] for o in outs]), ref.level)
+            assert np.array_equal(np.concatenate([o[0] for o in outs]), ref.parent)
+            assert [r.direction for r in res.trace] == [r.direction for r in ref.trace]
