@@ -525,17 +525,16 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
             }
         }
         if (Harvest) {
-            uint32_t ow[I];
+            // vis is complete (frontier committed before a barrier) and not
+            // written during the expansion: one read-only load per arc, then
+            // the parent update; the harvest pass derives the next frontier
+            // from parent != NIL.
 #pragma unroll
-            for (int k = 0; k < I; ++k) {
-                vw[k] = ok[k] ? (__ldg(&vis[v[k] >> 5]) | __ldg(&in[v[k] >> 5])) : ~0u;
-                ow[k] = ok[k] ? out[v[k] >> 5] : 0u;
-            }
+            for (int k = 0; k < I; ++k) vw[k] = ok[k] ? __ldg(&vis[v[k] >> 5]) : ~0u;
 #pragma unroll
             for (int k = 0; k < I; ++k) {
                 const uint32_t b = 1u << (v[k] & 31);
                 if (!(vw[k] & b)) {
-                    if (!(ow[k] & b)) atomicOr(&out[v[k] >> 5], b);
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
                 }
@@ -600,7 +599,7 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
                          const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
-    td_prologue(A, S, spare);
+    if (!Harvest) td_prologue(A, S, spare);  // harvest layers run it before a barrier
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
@@ -889,6 +888,60 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
     }
 }
 
+// Harvest after a fire-and-forget top-down expansion: a vertex was discovered
+// iff it was unvisited (vis, not written by the expansion) and has a parent
+// now.  Thread per word: parent loads for the word's unvisited non-isolated
+// vertices (one 128-byte line per word), next-frontier word and vis commit,
+// then the found vertices are stamped and appended like phase_convert.
+template <typename OffT>
+__device__ void phase_harvest(const Args<OffT> &A, const Queue<OffT> &Q, const Plane out,
+                              unsigned long long *counter, int32_t depth1, EnqSmem &es) {
+    const Plane vis{A.bits};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
+        const int64_t w = w0 + threadIdx.x;
+        uint32_t bits = 0;
+        if (w < A.nw) {
+            const uint32_t vw = vis[w];
+            uint32_t un = ~vw & __ldg(A.posw + w);
+            const uint32_t *pw = A.parent + w * 32;
+            while (un) {
+                const int b = __ffs(un) - 1;
+                un &= un - 1;
+                if (pw[b] != HBFS_NIL) bits |= 1u << b;
+            }
+            out[w] = bits;
+            if (bits) vis[w] = vw | bits;
+        }
+        while (__syncthreads_or(bits != 0)) {
+            bool has[kConvI];
+            uint32_t v[kConvI];
+            uint64_t deg[kConvI];
+            OffT r0[kConvI];
+#pragma unroll
+            for (int k = 0; k < kConvI; ++k) {
+                has[k] = bits != 0;
+                v[k] = 0;
+                deg[k] = 0;
+                r0[k] = 0;
+                if (has[k]) {
+                    v[k] = (uint32_t)(w * 32 + __ffs(bits) - 1);
+                    bits &= bits - 1;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kConvI; ++k) {
+                if (has[k]) {
+                    r0[k] = __ldg(A.rs + v[k]);
+                    deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - r0[k]);
+                    A.level[v[k]] = depth1;
+                }
+            }
+            block_enqueue<OffT, kConvI>(has, v, deg, r0, counter, Q, es);
+        }
+    }
+}
+
 // K: first-hit searches in flight per lane in the bottom-up phase;
 // MINB: CTAs per SM the register allocation must allow.
 // SCAN: also compile the 4-vector bottom-up path for tiny-frontier layers
@@ -958,12 +1011,17 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             if (harvest) phase_cb_run<OffT, true>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
             else phase_cb_run<OffT, false>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
         } else if (dir == HBFS_TOP_DOWN) {
-            if (harvest) phase_td<OffT, true>(A, S, in, out, spare, ctr, sm);
-            else phase_td<OffT, false>(A, S, in, out, spare, ctr, sm);
+            if (harvest) {
+                td_prologue(A, S, spare);
+                grid.sync();  // vis now holds the frontier: the expansion tests vis alone
+                phase_td<OffT, true>(A, S, in, out, spare, ctr, sm);
+            } else {
+                phase_td<OffT, false>(A, S, in, out, spare, ctr, sm);
+            }
         }
         if (harvest) {
             grid.sync();
-            phase_convert(A, A.qb[(L + 1) & 1], out, &ctr->packed, (int32_t)L + 1, true, sm.enq);
+            phase_harvest(A, A.qb[(L + 1) & 1], out, &ctr->packed, (int32_t)L + 1, sm.enq);
         }
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
