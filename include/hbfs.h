@@ -135,6 +135,12 @@ int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *level_dev,
                          int64_t *b_useful, void *stream);
 
 
+/* Diagnostics: per-layer barrier timestamps of the last traversal (8 slots of
+ * uint64 ns per layer: 0 layer start, 1 after bitmap->queue conversion, 2 after
+ * the top-down prologue barrier, 3 after a harvest layer's expansion, 4 end;
+ * 0 = phase not taken).  rows <= 1024. */
+int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows);
+
 /* ---- multi-GPU: one rank's share of a 1D vertex partition ----
  * Rank r owns vertices [lo, hi) (word aligned) with their CSR rows (global
  * column ids); frontier and visited bitmaps are replicated, parent/level owned.

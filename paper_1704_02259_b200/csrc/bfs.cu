@@ -48,6 +48,11 @@ constexpr int kLaneVecsScan = 4;
 constexpr int kPackShift = 35;               // packed counter: count<<35 | degree sum
 constexpr unsigned long long kPackMask = (1ull << kPackShift) - 1;
 constexpr int64_t kRowsCap = 1024;           // trace rows per launch
+constexpr int kPhaseSlots = 8;               // per-layer barrier timestamps kept for diagnostics
+// Frontier bitmaps live in a ring of kPlanes planes, one per depth, so levels
+// are stamped once at the end (one coalesced pass) instead of by scattered
+// stores at discovery; a plane reused in a deeper traversal is flushed first.
+constexpr int kPlanes = 32;
 // Column-blocked top-down (hub frontiers): frontier rows are split into
 // kCb ranges of target ids and processed range by range so the active slice
 // of parent/level/bitmaps/row-starts stays L2-resident.
@@ -126,9 +131,11 @@ struct Args {
     int64_t cb_range_len, cb_cs_stride, cb_min_arcs, harvest_min_arcs;
     Ctl *ctl;
     hbfs_layer_row *rows;
+    unsigned long long *phase_ns;  // kPhaseSlots timestamps per trace row (diagnostics)
     int64_t rows_cap;
     Heur H;
     int max_pos, use_simd, parent_mode, do_init;
+    int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
     uint32_t root;
 };
 
@@ -184,6 +191,32 @@ __device__ __forceinline__ int64_t block_grab(unsigned long long *work, int64_t 
     if (threadIdx.x == 0) *s_item = (int64_t)gridDim.x + (int64_t)atomicAdd(work, 1ull);
     __syncthreads();
     return *s_item;
+}
+
+template <typename A_t>
+__device__ __forceinline__ Plane depth_plane(const A_t &A, int64_t d) {
+    return Plane{A.bits + A.nw * (1 + d % kPlanes)};
+}
+
+// Clear the plane that layer L will use as `out` at L+1 (depth L+2), after
+// stamping the levels of the depth it held if the ring wrapped (deep graphs).
+template <typename A_t>
+__device__ __forceinline__ void clear_spare_word(const A_t &A, int64_t L, int64_t w) {
+    uint32_t *p = A.bits + A.nw * (1 + (L + 2) % kPlanes) + w;
+    if (L + 2 < kPlanes || A.direct_levels) {  // fresh plane / levels already stamped
+        *p = 0;
+        return;
+    }
+    uint32_t x = *p;
+    if (!x) return;
+    {
+        const int32_t d = (int32_t)(L + 2 - kPlanes);
+        while (x) {
+            A.level[w * 32 + __ffs(x) - 1] = d;
+            x &= x - 1;
+        }
+    }
+    *p = 0;
 }
 
 __device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
@@ -408,12 +441,12 @@ __device__ void phase_init(const Args<OffT> &A) {
     for (int64_t i = tid; i < A.n; i += nth) {
         const bool r = i == (int64_t)root;
         A.parent[i] = r ? root : HBFS_NIL;
-        A.level[i] = r ? 0 : -1;
+        if (A.direct_levels) A.level[i] = r ? 0 : -1;
     }
     // vis and B0 hold the root; B1, B2 zero
     const int64_t rw = root >> 5;
     const uint32_t rb = 1u << (root & 31);
-    for (int64_t w = tid; w < 4 * A.nw; w += nth)
+    for (int64_t w = tid; w < 3 * A.nw; w += nth)  // vis, depth plane 0 (root), plane 1
         A.bits[w] = (w == rw || w == A.nw + rw) ? rb : 0u;
     const OffT r0 = __ldg(A.rs + root);
     const uint64_t rdeg = (uint64_t)(__ldg(A.rs + root + 1) - r0);
@@ -453,7 +486,7 @@ __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare)
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Plane vis{A.bits};
-    for (int64_t w = tid; w < A.nw; w += nth) spare[w] = 0;
+    for (int64_t w = tid; w < A.nw; w += nth) clear_spare_word(A, S.layer, w);
     if (A.parent_mode != HBFS_PARENT_ANY) {
         for (int64_t i = tid; i < S.v_f; i += nth) {
             const uint32_t x = Q.q[i];
@@ -580,7 +613,7 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
             rsv[k] = 0;
             if (claim[k]) {
                 if (any_parent) A.parent[v[k]] = u[k];
-                A.level[v[k]] = depth1;
+                if (A.direct_levels) A.level[v[k]] = depth1;
                 rsv[k] = __ldg(A.rs + v[k]);
                 deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - rsv[k]);
             }
@@ -741,7 +774,6 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     const Plane vis{A.bits};
-    const int32_t depth1 = (int32_t)S.layer + 1;
     const int64_t max_pos = A.max_pos;
     // packed per-thread counters: found<<35 | their degree sum ; fallbacks<<35 | gathers
     unsigned long long c_fd = 0, c_fg = 0;
@@ -754,7 +786,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         const uint32_t vis0 = valid ? vis[wl] : ~0u;
         const uint32_t inl = valid ? in[wl] : 0u;
         const uint32_t pwl = valid ? __ldg(A.posw + wl) : 0u;
-        if (valid) spare[wl] = 0u;
+        if (valid) clear_spare_word(A, S.layer, wl);
         const uint32_t vwl = vis0 | inl;
         const uint32_t candl = ~vwl & pwl;
         if (valid && vwl != vis0) vis[wl] = vwl;  // commit a lagging frontier
@@ -806,7 +838,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 const bool early = found && pos < max_pos;
                 if (found) {
                     A.parent[v[k]] = hu[k];
-                    A.level[v[k]] = depth1;
+                    if (A.direct_levels) A.level[v[k]] = (int32_t)S.layer + 1;
                     atomicOr(&s_found[(v[k] >> 5) - tile * 32], 1u << (v[k] & 31));
                     c_fd += (1ull << kPackShift) + (unsigned long long)deg;
                 }
@@ -844,10 +876,69 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     __syncthreads();
 }
 
+// Word-level append: thread t contributes the vertices of bitmap word w (bits),
+// whose count and degree sum it computed; one CTA scan + one atomic reserves
+// the queue slots and arc range of all 512 words, then every thread writes its
+// entries (vertex, arc offset, row start) and the chunk starts inside its arc
+// range in order.  Optionally stamps level = stamp.  Block-uniform call.
+template <typename OffT>
+__device__ __forceinline__ void word_enqueue(const Args<OffT> &A, const Queue<OffT> &Q, int64_t w,
+                                             uint32_t bits, uint32_t cnt, uint64_t dsum,
+                                             unsigned long long *counter, int32_t stamp,
+                                             EnqSmem &es) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = ((unsigned long long)cnt << kPackShift) + dsum;  // packed, inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(full, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) es.wtot[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            const unsigned long long t = es.wtot[k];
+            es.wtot[k] = run;
+            run += t;
+        }
+        es.wbase[0] = run ? atomicAdd(counter, run) : 0ull;
+    }
+    __syncthreads();
+    if (!cnt) return;
+    const unsigned long long mine = ((unsigned long long)cnt << kPackShift) + dsum;
+    const unsigned long long base = es.wbase[0] + es.wtot[wid] + (x - mine);
+    uint64_t pos = base >> kPackShift, off = base & kPackMask;
+    while (bits) {
+        const uint32_t v = (uint32_t)(w * 32 + __ffs(bits) - 1);
+        bits &= bits - 1;
+        const OffT r0 = __ldg(A.rs + v);
+        const uint64_t d = (uint64_t)(__ldg(A.rs + v + 1) - r0);
+        Q.q[pos] = v;
+        Q.qo[pos] = (OffT)off;
+        Q.qr[pos] = r0;
+        for (uint64_t c = (off + kTdChunk - 1) / kTdChunk; c * kTdChunk < off + d; ++c)
+            Q.cs[c] = (uint32_t)pos;
+        ++pos;
+        off += d;
+    }
+}
+
+// degree sum of the vertices of word w in `bits`
+template <typename OffT>
+__device__ __forceinline__ uint64_t word_degsum(const Args<OffT> &A, int64_t w, uint32_t bits) {
+    uint64_t d = 0;
+    while (bits) {
+        const uint32_t v = (uint32_t)(w * 32 + __ffs(bits) - 1);
+        bits &= bits - 1;
+        d += (uint64_t)(__ldg(A.rs + v + 1) - __ldg(A.rs + v));
+    }
+    return d;
+}
+
 // Bitmap -> queue (with arc prefix, row starts, chunk starts) at a bottom-up ->
-// top-down switch.  Thread per frontier word; each round every thread peels up
-// to kConvI vertices off its word and the CTA appends them with one atomic.
-constexpr int kConvI = 4;
+// top-down switch: thread per frontier word, word_enqueue per 512 words.
 
 template <typename OffT>
 __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const Plane bm,
@@ -857,34 +948,9 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
         const int64_t w = w0 + threadIdx.x;
-        uint32_t bits = w < A.nw ? bm[w] : 0u;
+        const uint32_t bits = w < A.nw ? bm[w] : 0u;
         if (commit_vis && bits) vis[w] |= bits;
-        while (__syncthreads_or(bits != 0)) {
-            bool has[kConvI];
-            uint32_t v[kConvI];
-            uint64_t deg[kConvI];
-            OffT r0[kConvI];
-#pragma unroll
-            for (int k = 0; k < kConvI; ++k) {
-                has[k] = bits != 0;
-                v[k] = 0;
-                deg[k] = 0;
-                r0[k] = 0;
-                if (has[k]) {
-                    v[k] = (uint32_t)(w * 32 + __ffs(bits) - 1);
-                    bits &= bits - 1;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < kConvI; ++k) {
-                if (has[k]) {
-                    r0[k] = __ldg(A.rs + v[k]);
-                    deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - r0[k]);
-                    if (stamp_level) A.level[v[k]] = stamp_level;
-                }
-            }
-            block_enqueue<OffT, kConvI>(has, v, deg, r0, counter, Q, es);
-        }
+        word_enqueue(A, Q, w, bits, __popc(bits), word_degsum(A, w, bits), counter, stamp_level, es);
     }
 }
 
@@ -894,50 +960,76 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
 // vertices (one 128-byte line per word), next-frontier word and vis commit,
 // then the found vertices are stamped and appended like phase_convert.
 template <typename OffT>
-__device__ void phase_harvest(const Args<OffT> &A, const Queue<OffT> &Q, const Plane out,
-                              unsigned long long *counter, int32_t depth1, EnqSmem &es) {
+__device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
+                              unsigned long long *red, int32_t depth1) {
     const Plane vis{A.bits};
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
-        const int64_t w = w0 + threadIdx.x;
-        uint32_t bits = 0;
-        if (w < A.nw) {
-            const uint32_t vw = vis[w];
-            uint32_t un = ~vw & __ldg(A.posw + w);
-            const uint32_t *pw = A.parent + w * 32;
-            while (un) {
-                const int b = __ffs(un) - 1;
-                un &= un - 1;
-                if (pw[b] != HBFS_NIL) bits |= 1u << b;
-            }
-            out[w] = bits;
-            if (bits) vis[w] = vw | bits;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long acc = 0;  // packed count<<35 | degree sum
+    for (int64_t w = tid; w < A.nw; w += nth) {
+        const uint32_t vw = vis[w];
+        uint32_t un = ~vw & __ldg(A.posw + w), bits = 0;
+        const uint32_t *pw = A.parent + w * 32;
+        while (un) {
+            const int b = __ffs(un) - 1;
+            un &= un - 1;
+            if (pw[b] != HBFS_NIL) bits |= 1u << b;
         }
-        while (__syncthreads_or(bits != 0)) {
-            bool has[kConvI];
-            uint32_t v[kConvI];
-            uint64_t deg[kConvI];
-            OffT r0[kConvI];
+        out[w] = bits;
+        if (bits) {
+            vis[w] = vw | bits;
+            acc += ((unsigned long long)__popc(bits) << kPackShift) + word_degsum(A, w, bits);
+            if (A.direct_levels)
+                for (uint32_t x = bits; x; x &= x - 1) A.level[w * 32 + __ffs(x) - 1] = depth1;
+        }
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        if (t) atomicAdd(counter, t);
+    }
+    __syncthreads();
+}
+
+// Final level stamp: level[v] = the depth plane holding v (unflushed depths
+// d0..nL-1), -1 if never visited; vertices of flushed depths keep the level
+// written when their plane was recycled.
+template <typename OffT>
+__device__ void phase_levels(const Args<OffT> &A, int64_t nL) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t d0 = nL + 2 - kPlanes > 0 ? nL + 2 - kPlanes : 0;
+    // thread per word: its depth-plane words (coalesced across the warp), then
+    // its 32 levels as eight 16-byte stores
+    for (int64_t w = tid; w < A.nw; w += nth) {
+        const uint32_t vw = A.bits[w];
+        const bool full_word = (w + 1) * 32 <= A.n;
+        int32_t lv[32];
 #pragma unroll
-            for (int k = 0; k < kConvI; ++k) {
-                has[k] = bits != 0;
-                v[k] = 0;
-                deg[k] = 0;
-                r0[k] = 0;
-                if (has[k]) {
-                    v[k] = (uint32_t)(w * 32 + __ffs(bits) - 1);
-                    bits &= bits - 1;
-                }
-            }
+        for (int b = 0; b < 32; ++b) lv[b] = ((vw >> b) & 1u) ? -2 : -1;  // -2: visited, flushed
+        for (int64_t g0 = d0; g0 < nL; g0 += 8) {
+            uint32_t p[8];
 #pragma unroll
-            for (int k = 0; k < kConvI; ++k) {
-                if (has[k]) {
-                    r0[k] = __ldg(A.rs + v[k]);
-                    deg[k] = (uint64_t)(__ldg(A.rs + v[k] + 1) - r0[k]);
-                    A.level[v[k]] = depth1;
-                }
+            for (int j = 0; j < 8; ++j) p[j] = g0 + j < nL ? depth_plane(A, g0 + j)[w] : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                for (int b = 0; b < 32; ++b)
+                    if ((p[j] >> b) & 1u) lv[b] = (int32_t)(g0 + j);
             }
-            block_enqueue<OffT, kConvI>(has, v, deg, r0, counter, Q, es);
+        }
+        int32_t *dst = A.level + w * 32;
+        if (full_word && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && d0 == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                reinterpret_cast<int4 *>(dst)[q] =
+                    make_int4(lv[4 * q], lv[4 * q + 1], lv[4 * q + 2], lv[4 * q + 3]);
+        } else {
+            for (int b = 0; b < 32; ++b)
+                if (w * 32 + b < A.n && lv[b] != -2) dst[b] = lv[b];
         }
     }
 }
@@ -956,9 +1048,12 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
 
     St S;
+    unsigned long long *kstamp = A.phase_ns + kRowsCap * kPhaseSlots;  // kernel-level marks
+    if (leader) kstamp[0] = globaltimer();
     if (A.do_init) {
         phase_init(A);
         grid.sync();
+        if (leader) kstamp[1] = globaltimer();
         const int64_t rdeg = (int64_t)(__ldg(A.rs + A.root + 1) - __ldg(A.rs + A.root));
         S.layer = 0;
         S.v_f = 1;
@@ -982,16 +1077,22 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
 
     int64_t rows = 0;
     uint64_t t_start = leader ? globaltimer() : 0;
+#define STAMP(k) \
+    if (leader) A.phase_ns[rows * kPhaseSlots + (k)] = globaltimer()
     while (S.v_f > 0 && rows < A.rows_cap) {
+        if (leader)
+            for (int k = 0; k < kPhaseSlots; ++k) A.phase_ns[rows * kPhaseSlots + k] = 0;
+        STAMP(0);
         int64_t fv, gv;
         const int dir = decide(A.H, S.dir, S.v_f, S.e_f, S.eu_v, S.eu_e, S.prev_vf, &fv, &gv);
         const int64_t L = S.layer;
-        const Plane in{A.bits + A.nw * (1 + L % 3)}, out{A.bits + A.nw * (1 + (L + 1) % 3)},
-            spare{A.bits + A.nw * (1 + (L + 2) % 3)};
+        const Plane in = depth_plane(A, L), out = depth_plane(A, L + 1),
+                    spare = depth_plane(A, L + 2);
         Ctr *ctr = &A.ctl->ctr[L % 3];
         if (dir == HBFS_TOP_DOWN && S.kind == 1) {
             phase_convert(A, A.qb[L & 1], in, &A.ctl->conv, 0, false, sm.enq);
             grid.sync();
+            STAMP(1);
         }
         const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && S.e_f >= A.cb_min_arcs &&
                         S.v_f <= kCbMaxF;
@@ -1008,12 +1109,14 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         if (cb) {
             phase_cb_build(A, S, spare, (int)(L & 1));
             grid.sync();
+            STAMP(2);
             if (harvest) phase_cb_run<OffT, true>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
             else phase_cb_run<OffT, false>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
         } else if (dir == HBFS_TOP_DOWN) {
             if (harvest) {
                 td_prologue(A, S, spare);
                 grid.sync();  // vis now holds the frontier: the expansion tests vis alone
+                STAMP(2);
                 phase_td<OffT, true>(A, S, in, out, spare, ctr, sm);
             } else {
                 phase_td<OffT, false>(A, S, in, out, spare, ctr, sm);
@@ -1021,7 +1124,8 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         }
         if (harvest) {
             grid.sync();
-            phase_harvest(A, A.qb[(L + 1) & 1], out, &ctr->packed, (int32_t)L + 1, sm.enq);
+            STAMP(3);
+            phase_harvest(A, out, &ctr->packed, red, (int32_t)L + 1);
         }
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
@@ -1031,6 +1135,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         }
         grid.sync();
 
+        STAMP(4);
         const unsigned long long packed = __ldcg(&ctr->packed);
         const int64_t nvf = (int64_t)(packed >> kPackShift);
         const int64_t nef = (int64_t)(packed & kPackMask);
@@ -1064,9 +1169,17 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         S.eu_v -= nvf;
         S.eu_e -= nef;
         S.dir = dir;
-        S.kind = dir == HBFS_TOP_DOWN ? 0 : 1;
+        S.kind = (dir == HBFS_TOP_DOWN && !harvest) ? 0 : 1;  // harvest builds no queue
         S.layer = L + 1;
         ++rows;
+    }
+    if (leader) kstamp[2] = globaltimer();
+    if (S.v_f == 0 && !A.direct_levels) {  // finished in this launch: stamp the levels
+        grid.sync();
+        if (leader) kstamp[3] = globaltimer();
+        phase_levels(A, S.layer);
+        grid.sync();
+        if (leader) kstamp[4] = globaltimer();
     }
     if (leader) {
         Ctl *c = A.ctl;
@@ -1127,6 +1240,7 @@ struct Workspace {
     int64_t n = 0;
     int wide = 0;
     DevBuf parent, level, bits, q, qo, qr, cs, ctl;  // ctl: Ctl followed by kRowsCap rows
+    DevBuf phases;  // kRowsCap * kPhaseSlots barrier timestamps (last launch)
     DevBuf cbq, cbqo, cbqr, cbcs;  // column-blocked top-down segment queues
     int cb_ranges = 0;
     int64_t ncs = 0;  // chunk-start entries per queue buffer
@@ -1152,7 +1266,7 @@ static int ws_alloc(hbfs_graph *g) {
     if (!rc) rc = w->parent.alloc(n * 4);
     if (!rc) rc = w->level.alloc(n * 4);
     w->ncs = g->arcs / kTdChunk + 2;
-    if (!rc) rc = w->bits.alloc(4 * nw * 4 + 64);
+    if (!rc) rc = w->bits.alloc((1 + kPlanes) * nw * 4 + 64);
     if (!rc) rc = w->q.alloc(2 * (n + 1) * 4 + 16);
     if (!rc) rc = w->qo.alloc(2 * (n + 1) * sizeof(OffT));
     if (!rc) rc = w->qr.alloc(2 * (n + 1) * sizeof(OffT));
@@ -1170,6 +1284,7 @@ static int ws_alloc(hbfs_graph *g) {
         if (!rc) rc = w->cbcs.alloc(P * w->ncs * 4);
     }
     if (!rc) rc = w->ctl.alloc(ctl_bytes());
+    if (!rc) rc = w->phases.alloc((kRowsCap + 1) * kPhaseSlots * 8);
     if (!rc && cudaMallocHost(&w->h_ctl, ctl_bytes()) != cudaSuccess)
         rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
     if (!rc && (cudaEventCreate(&w->ev0) != cudaSuccess || cudaEventCreate(&w->ev1) != cudaSuccess))
@@ -1221,6 +1336,9 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.cb_cs_stride = w->ncs;
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
     A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
+    // level arrays that fit L2 take scattered stores cheaply; larger graphs
+    // stamp levels once from the depth planes (HBFS_DEFER_LEVELS_MIN_N: test knob)
+    A.direct_levels = g->n < env_i64("HBFS_DEFER_LEVELS_MIN_N", int64_t(1) << 22);
     A.cbq.q = w->cbq.as<uint32_t>();
     A.cbq.qo = w->cbqo.as<OffT>();
     A.cbq.qr = w->cbqr.as<OffT>();
@@ -1234,6 +1352,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.ctl = w->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(w->ctl.as<char>() + sizeof(Ctl));
     A.rows_cap = kRowsCap;
+    A.phase_ns = w->phases.as<unsigned long long>();
     A.H.heuristic = p->heuristic;
     A.H.counter_mode = p->counter_mode;
     A.H.force = p->force_direction;
@@ -1311,5 +1430,20 @@ extern "C" int hbfs_bfs(hbfs_graph *g, int64_t root, const hbfs_params *p, uint3
                                  n_layers, device_ms, st);
     return run_bfs<uint32_t>(g, (uint32_t)root, p, parent, level, on_device, trace, trace_cap,
                              n_layers, device_ms, st);
+    HB_ENTRY_END
+}
+
+// Diagnostics: per-layer barrier timestamps (ns, device globaltimer) of the last
+// launch of the last traversal: slot 0 layer start, 1 after the bitmap->queue
+// conversion, 2 after the top-down prologue barrier, 3 after the expansion
+// (harvest layers), 4 layer end; 0 = phase not taken.
+extern "C" int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows) {
+    HB_ENTRY_BEGIN
+    using namespace hbfs;
+    if (!g || !out || rows < 0) return set_error(HBFS_EINVAL, "bad arguments");
+    if (!g->ws) return set_error(HBFS_EINVAL, "no traversal yet");
+    if (rows > kRowsCap + 1) rows = kRowsCap + 1;
+    HB_CUDA(cudaMemcpy(out, g->ws->phases.p, rows * kPhaseSlots * 8, cudaMemcpyDeviceToHost));
+    return HBFS_OK;
     HB_ENTRY_END
 }

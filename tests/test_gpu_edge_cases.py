@@ -93,8 +93,12 @@ def test_high_degree_hub_long_rows(cuda, oracle):
     check_all(hb, oracle, pairs, n, roots=[0, 1, 2500, 4999])
 
 
-def test_deep_path_resumes_across_launches(cuda, oracle):
-    # 3000 layers > the per-launch trace capacity: exercises the persisted state
+@pytest.mark.parametrize("defer", [False, True])
+def test_deep_path_resumes_across_launches(cuda, oracle, monkeypatch, defer):
+    # 3000 layers > the per-launch trace capacity: exercises the persisted state;
+    # with deferred level stamping the 32-plane depth ring wraps ~100 times
+    if defer:
+        monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
     hb = cuda
     n = 3000
     pairs = [(i, i + 1) for i in range(n - 1)]
@@ -183,10 +187,12 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
     import os
 
     hb = cuda
-    keys = ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES", "HBFS_HARVEST_MIN_ARCS")
+    keys = ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES", "HBFS_HARVEST_MIN_ARCS",
+            "HBFS_DEFER_LEVELS_MIN_N")
     old = {k: os.environ.get(k) for k in keys}
     os.environ.update(HBFS_CB_MIN_N="0" if cb else str(1 << 40), HBFS_CB_MIN_ARCS="0",
-                      HBFS_CB_RANGES="7", HBFS_HARVEST_MIN_ARCS="0" if harvest else str(1 << 40))
+                      HBFS_CB_RANGES="7", HBFS_HARVEST_MIN_ARCS="0" if harvest else str(1 << 40),
+                      HBFS_DEFER_LEVELS_MIN_N="0" if harvest else str(1 << 40))
     try:
         for meta in golden_hashes["small"]:
             name = meta["name"]

@@ -78,8 +78,11 @@ def test_device_generator_and_csr(cuda, small_golden, small_graphs, name):
     assert np.array_equal(hb.sample_sources(g, 8, 1), small_golden[f"{name}/sources"])
 
 
+@pytest.mark.parametrize("defer", [False, True])
 @pytest.mark.parametrize("name", SMALL)
-def test_traversals_match_reference(cuda, small_golden, small_graphs, name):
+def test_traversals_match_reference(cuda, small_golden, small_graphs, name, defer, monkeypatch):
+    if defer:  # deferred level stamping (depth planes + final pass), normally n >= 2^22
+        monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
     hb = cuda
     _, g = small_graphs[name]
     for s in small_golden[f"{name}/sources"]:

@@ -13,6 +13,7 @@ ap.add_argument("--heuristic", default="beamer")
 ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--parent-mode", default="minid")
 ap.add_argument("--root", type=int, default=-1)
+ap.add_argument("--phases", action="store_true")
 a = ap.parse_args()
 probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
 t0 = time.time()
@@ -34,5 +35,19 @@ for s in roots:
     if not a.quiet:
         lay = " ".join(f"{"B" if x.direction=="bottom-up" else "T"}{x.v_f}[{x.e_f/1e6:.1f}M]:{x.elapsed*1e6:.1f}us" for x in r.trace)
         print(f"root {int(s)}: {r.device_seconds*1e6:.1f}us  sum(layers)={sum(x.elapsed for x in r.trace)*1e6:.1f}us  {lay}", flush=True)
+        if a.phases:
+            import ctypes as C
+            from paper_1704_02259_b200 import _lib
+            nl = len(r.trace)
+            buf = np.zeros(nl * 8, dtype=np.uint64)
+            _lib.check(_lib.load().hbfs_phase_times(g.handle, buf.ctypes.data_as(C.c_void_p), nl))
+            kb = np.zeros(1025 * 8, dtype=np.uint64)
+            _lib.check(_lib.load().hbfs_phase_times(g.handle, kb.ctypes.data_as(C.c_void_p), 1025))
+            k = kb[1024 * 8:1024 * 8 + 8].astype(np.int64)
+            print(f"   kernel: init {(k[1]-k[0])/1e3:.1f}us  layers {(k[2]-k[1])/1e3:.1f}us  final-sync {(k[3]-k[2])/1e3:.1f}us  levels {(k[4]-k[3])/1e3:.1f}us")
+            for i, x in enumerate(r.trace):
+                t = buf[i * 8:(i + 1) * 8].astype(np.int64)
+                marks = [(k, t[k] - t[0]) for k in (1, 2, 3, 4) if t[k]]
+                print(f"   L{i} {x.direction[0].upper()} v_f={x.v_f} e_f={x.e_f}: " + " ".join(f"s{k}@{v/1e3:.1f}us" for k, v in marks))
 m = g.in_edges_total
 print(f"hmean GTEPS {len(tot)*m/sum(tot)/1e9:.2f}  mean us {np.mean(tot)*1e6:.1f}")
