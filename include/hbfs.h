@@ -135,6 +135,11 @@ int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *level_dev,
                          int64_t *b_useful, void *stream);
 
 
+/* Same accounting, B_sector of every layer separately (init bytes excluded). */
+int hbfs_traversal_bytes_layers(hbfs_graph *g, int64_t root, const int32_t *level_dev,
+                                const int32_t *directions, int64_t n_layers,
+                                int64_t *b_sector_per_layer, void *stream);
+
 /* Diagnostics: per-layer barrier timestamps of the last traversal (8 slots of
  * uint64 ns per layer: 0 layer start, 1 after bitmap->queue conversion, 2 after
  * the top-down prologue barrier, 3 after a harvest layer's expansion, 4 end;

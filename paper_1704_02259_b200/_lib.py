@@ -68,6 +68,7 @@ SIGNATURES = {
     "hbfs_validate": (C.c_int, [P, i64, P, P, C.c_int, C.c_int, P, P, P]),
     "hbfs_traversal_bytes": (C.c_int, [P, i64, P, P, i64, P, P, P]),
     "hbfs_phase_times": (C.c_int, [P, P, i64]),
+    "hbfs_traversal_bytes_layers": (C.c_int, [P, i64, P, P, i64, P, P]),
     # multi-GPU partition (csrc/part.cu)
     "hbfs_part_build": (C.c_int, [P, P, i64, i64, i64, i64, C.c_int, C.c_int, P, C.POINTER(P)]),
     "hbfs_part_from_csr": (C.c_int, [P, P, i64, i64, i64, i64, P, C.POINTER(P)]),

@@ -365,7 +365,7 @@ __global__ void k_popc(const uint32_t *f, int64_t words, unsigned long long *out
 template <typename OffT>
 static int bytes_impl(hbfs_graph *g, int64_t root, const int32_t *level,
                       const int32_t *dirs, int64_t n_layers, int64_t *b_sector, int64_t *b_useful,
-                      cudaStream_t st) {
+                      int64_t *per_layer, cudaStream_t st) {
     const int64_t n = g->n, nw = g->nw, arcs = g->arcs;
     const int rs_bytes = sizeof(OffT);
     const OffT *rs = g->rs.as<OffT>();
@@ -415,6 +415,7 @@ static int bytes_impl(hbfs_graph *g, int64_t root, const int32_t *level,
         // parent[N] and level[N] have identical sector sets (both 4 B per vertex)
         const int64_t s_rs = hp[0] * 32, s_adj = hp[1] * 32, s_bm = hp[2] * 32, s_pl = 2 * hp[3] * 32;
         const int64_t N = (int64_t)hc[2];
+        const int64_t bs_before = bs;
         if (dirs[L] == HBFS_TOP_DOWN) {
             const int64_t F = (int64_t)hc[0], mf = (int64_t)hc[1];
             bs += sec(4 * F) + s_rs + s_adj + s_bm + s_pl + sec(4 * N);
@@ -424,6 +425,7 @@ static int bytes_impl(hbfs_graph *g, int64_t root, const int32_t *level,
             bs += 4 * W + s_rs + s_adj + s_bm + s_pl + 4 * W;
             bu += 8 * W + 8 * U + 4 * probes + 8 * N;
         }
+        if (per_layer) per_layer[L] = bs - bs_before;
     }
     *b_sector = bs;
     *b_useful = bu;
@@ -469,7 +471,26 @@ extern "C" int hbfs_traversal_bytes(hbfs_graph *g, int64_t root, const int32_t *
         return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (g->wide)
-        return bytes_impl<uint64_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful, st);
-    return bytes_impl<uint32_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful, st);
+        return bytes_impl<uint64_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful,
+                                    nullptr, st);
+    return bytes_impl<uint32_t>(g, root, level_dev, directions, n_layers, b_sector, b_useful,
+                                nullptr, st);
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_traversal_bytes_layers(hbfs_graph *g, int64_t root, const int32_t *level_dev,
+                                           const int32_t *directions, int64_t n_layers,
+                                           int64_t *b_sector_per_layer, void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!g || !level_dev || !directions || !b_sector_per_layer)
+        return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int64_t bs = 0, bu = 0;
+    if (g->wide)
+        return bytes_impl<uint64_t>(g, root, level_dev, directions, n_layers, &bs, &bu,
+                                    b_sector_per_layer, st);
+    return bytes_impl<uint32_t>(g, root, level_dev, directions, n_layers, &bs, &bu,
+                                b_sector_per_layer, st);
     HB_ENTRY_END
 }

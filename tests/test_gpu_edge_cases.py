@@ -216,3 +216,27 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+def test_large_graph_kernel_variant_on_small_graphs(cuda, small_golden, golden_hashes, monkeypatch):
+    """The SCALE>=24 kernel variant (2 CTAs/SM, tiny-frontier scan path with the
+    shared-memory frontier summary) forced on the golden small graphs."""
+    hb = cuda
+    monkeypatch.setenv("HBFS_KERNEL_VARIANT", "3")
+    for meta in golden_hashes["small"]:
+        name = meta["name"]
+        p = dict(meta["params"])
+        if "probs" in p:
+            p["probs"] = tuple(p["probs"])
+        g = hb.generate_graph(hb.GraphParams(**p))  # fresh workspace picks the variant
+        for s in small_golden[f"{name}/sources"]:
+            s = int(s)
+            for mode, kw in (("simd_default", dict(use_simd=True)),
+                             ("force_bu", dict(use_simd=True, force_direction="bottom-up")),
+                             ("simd_maxpos3", dict(use_simd=True, cfg=hb.VecConfig(max_pos=3)))):
+                r = hb.bfs(g, s, device=False, **kw)
+                assert np.array_equal(r.level, small_golden[f"{name}/{s}/level"]), (name, s, mode)
+                assert np.array_equal(r.parent, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
+                tr = np.array([[x.layer, 1 if x.direction == "bottom-up" else 0, x.v_f, x.e_f, x.e_u,
+                                x.f_value, x.g_value, x.fallback_count, x.gather_count] for x in r.trace])
+                assert np.array_equal(tr, small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)

@@ -45,8 +45,13 @@ for s in roots:
             _lib.check(_lib.load().hbfs_phase_times(g.handle, kb.ctypes.data_as(C.c_void_p), 1025))
             k = kb[1024 * 8:1024 * 8 + 8].astype(np.int64)
             print(f"   kernel: init {(k[1]-k[0])/1e3:.1f}us  layers {(k[2]-k[1])/1e3:.1f}us  final-sync {(k[3]-k[2])/1e3:.1f}us  levels {(k[4]-k[3])/1e3:.1f}us")
+            dirs = np.array([1 if x.direction == "bottom-up" else 0 for x in r.trace], dtype=np.int32)
+            pl = np.zeros(nl, dtype=np.int64)
+            _lib.check(_lib.load().hbfs_traversal_bytes_layers(g.handle, int(s), C.c_void_p(lev.data_ptr()),
+                       dirs.ctypes.data_as(C.c_void_p), nl, pl.ctypes.data_as(C.c_void_p), None))
             for i, x in enumerate(r.trace):
                 t = buf[i * 8:(i + 1) * 8].astype(np.int64)
+                print(f"     B_sector {pl[i]/1e6:.1f} MB -> {pl[i]/max(x.elapsed,1e-9)/1e9:.0f} GB/s", end="")
                 marks = [(k, t[k] - t[0]) for k in (1, 2, 3, 4) if t[k]]
                 print(f"   L{i} {x.direction[0].upper()} v_f={x.v_f} e_f={x.e_f}: " + " ".join(f"s{k}@{v/1e3:.1f}us" for k, v in marks))
 m = g.in_edges_total
