@@ -505,19 +505,20 @@ __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare)
 // a vertex unvisited before the layer does RED.OR on its next-frontier bit and
 // RED.MIN (min-id) or a plain store (any) on its parent; levels, counters and
 // the next queue come from a word-order harvest of the bitmap afterwards.
-template <typename OffT, bool Harvest>
+// SPAN: base chunks (of kTdChunk arcs) per work item; harvest layers use 2.
+template <typename OffT, bool Harvest, int SPAN>
 __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
                                          uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
                                          const Plane in, const Plane out, const Queue<OffT> &NQ,
                                          Ctr *ctr, TdSmem<OffT> &sm) {
-    constexpr int I = kTdItems;
+    constexpr int I = kTdItems * SPAN;
     const Plane vis{A.bits};
     const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
         const uint64_t a0 = (uint64_t)c * kTdChunk;
-        const uint64_t a1 = min(a0 + (uint64_t)kTdChunk, mf);
+        const uint64_t a1 = min(a0 + (uint64_t)kTdChunk * SPAN, mf);
         if (threadIdx.x == 0) {
             const int64_t q0 = Q.cs[c];
-            const int64_t ql = (c + 1 < nchunks) ? (int64_t)Q.cs[c + 1] : nf - 1;
+            const int64_t ql = (c + SPAN < nchunks) ? (int64_t)Q.cs[c + SPAN] : nf - 1;
             sm.q0 = q0;
             sm.cnt = ql - q0 + 1;
         }
@@ -635,10 +636,13 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
     if (!Harvest) td_prologue(A, S, spare);  // harvest layers run it before a barrier
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
+    constexpr int SPAN = Harvest ? 2 : 1;
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
+    const int64_t nitems = (nchunks + SPAN - 1) / SPAN;
     unsigned long long *work = &A.ctl->work[S.layer % 3];
-    for (int64_t c = blockIdx.x; c < nchunks; c = block_grab(work, &sm.item))
-        td_chunk<OffT, Harvest>(A, Q, nf, mf, c, nchunks, (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
+    for (int64_t g = blockIdx.x; g < nitems; g = block_grab(work, &sm.item))
+        td_chunk<OffT, Harvest, SPAN>(A, Q, nf, mf, g * SPAN, nchunks, (int32_t)S.layer + 1, in, out,
+                                      NQ, ctr, sm);
 }
 
 template <typename OffT>
@@ -705,12 +709,14 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
                              Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre) {
     const int P = A.cb_ranges;
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
-    if (threadIdx.x == 0) {
+    constexpr int SPAN = Harvest ? 2 : 1;
+    if (threadIdx.x == 0) {  // prefix of work items (SPAN base chunks each) over ranges
         int64_t run = 0;
         for (int r = 0; r < P; ++r) {
             s_pre[r] = run;
             const unsigned long long t = __ldcg(&A.ctl->cbctr[bank][r]);
-            run += (int64_t)(((t & kPackMask) + kTdChunk - 1) / kTdChunk);
+            const int64_t nch = (int64_t)(((t & kPackMask) + kTdChunk - 1) / kTdChunk);
+            run += (nch + SPAN - 1) / SPAN;
         }
         s_pre[P] = run;
     }
@@ -724,7 +730,8 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
         const int64_t nf_r = (int64_t)(t >> kPackShift);
         const uint64_t mf_r = t & kPackMask;
         const Queue<OffT> R = cb_queue(A, r, kCbMaxF);
-        td_chunk<OffT, Harvest>(A, R, nf_r, mf_r, g - s_pre[r], s_pre[r + 1] - s_pre[r], (int32_t)S.layer + 1,
+        const int64_t nch_r = (int64_t)((mf_r + kTdChunk - 1) / kTdChunk);
+        td_chunk<OffT, Harvest, SPAN>(A, R, nf_r, mf_r, (g - s_pre[r]) * SPAN, nch_r, (int32_t)S.layer + 1,
                  in, out, NQ, ctr, sm);
     }
 }
