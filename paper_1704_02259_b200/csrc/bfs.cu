@@ -751,7 +751,7 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
 // no atomics, short layers spread over all warps), then dynamic grabs of kGrab
 // consecutive tiles from a per-layer counter (balances long layers).
 struct TileSched {
-    static constexpr int64_t kGrab = 4;
+    static constexpr int64_t kGrab = 1;
     unsigned long long *work;
     int64_t tile, nwarps, k = 0, dyn_end = -1;
     __device__ TileSched(unsigned long long *w, int64_t warp, int64_t nw)
