@@ -13,6 +13,7 @@ Host copies of ``row_starts`` / ``adjacency`` are exported lazily.
 from __future__ import annotations
 
 import ctypes as C
+import struct
 
 import numpy as np
 
@@ -163,3 +164,54 @@ _IMPORTED: dict = {}
 
 def degree(g: CsrGraph, v: int) -> int:
     return g.degree(v)
+
+
+# ---------------------------------------------------------------- CSR cache
+# a CSR blob next to the reference's HBFSEDG1 edge-list dump
+# (generator.py:162-187), so large graphs are built once.  Layout (little
+# endian): magic "HBFSCSR1", header <QQQIIQ8d> = n, arcs, m_edges, scale,
+# flags (bit0 dedup, bit1 permute_labels), seed, edgefactor, probs[4] and 3
+# reserved doubles; then int64 row_starts[n+1], uint32 adjacency[arcs].
+
+_CSR_MAGIC = b"HBFSCSR1"
+_CSR_HEADER = struct.Struct("<8sQQQIIQd4d3d")
+
+
+def save(g, path, params: GraphParams | None = None, dedup: bool = False) -> None:
+    """Write the CSR of `g` (our CsrGraph or any object with the reference
+    CsrGraph fields) to `path`."""
+    rs = np.ascontiguousarray(g.row_starts, dtype=np.int64)
+    adj = np.ascontiguousarray(g.adjacency, dtype=np.uint32)
+    n = len(rs) - 1
+    m = int(getattr(g, "in_edges_total", len(adj) // 2))
+    probs = tuple(params.probs) if params else (0.0, 0.0, 0.0, 0.0)
+    flags = (1 if dedup else 0) | (2 if (params is None or params.permute_labels) else 0)
+    with open(path, "wb") as fh:
+        fh.write(_CSR_HEADER.pack(_CSR_MAGIC, n, len(adj), m, params.scale if params else 0, flags,
+                                  params.seed if params else 0,
+                                  float(params.edgefactor) if params else 0.0, *probs, 0.0, 0.0, 0.0))
+        rs.tofile(fh)
+        adj.tofile(fh)
+
+
+def load_arrays(path):
+    """Read a CSR blob -> (row_starts, adjacency, m_edges, meta dict)."""
+    with open(path, "rb") as fh:
+        hdr = _CSR_HEADER.unpack(fh.read(_CSR_HEADER.size))
+        if hdr[0] != _CSR_MAGIC:
+            raise ValueError(f"bad magic {hdr[0]!r}")
+        n, arcs, m, scale, flags, seed, ef = hdr[1:8]
+        probs = tuple(hdr[8:12])
+        rs = np.fromfile(fh, dtype="<i8", count=n + 1)
+        adj = np.fromfile(fh, dtype="<u4", count=arcs)
+    if len(rs) != n + 1 or len(adj) != arcs or int(rs[-1]) != arcs:
+        raise ValueError("truncated or inconsistent CSR blob")
+    meta = dict(scale=scale, dedup=bool(flags & 1), permute_labels=bool(flags & 2), seed=seed,
+                edgefactor=int(ef), probs=probs)
+    return rs, adj, int(m), meta
+
+
+def load(path) -> CsrGraph:
+    """CSR blob -> device graph."""
+    rs, adj, m, _ = load_arrays(path)
+    return from_csr(rs, adj, m)

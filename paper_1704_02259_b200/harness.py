@@ -187,20 +187,41 @@ def run_benchmark(params: GraphParams, mode: str = "scalar-hybrid",
                   heuristic: HeuristicParams | None = None, cfg: VecConfig | None = None,
                   runs: int = 64, allow_isolated: bool = False, engine_name: str = "auto",
                   source_seed: int | None = None, dedup: bool = False,
-                  parent_mode: str = "minid") -> BenchmarkReport:
-    """Generate, build, then time ``runs`` traversals with validation (harness.py:247-296)."""
+                  parent_mode: str = "minid", csr_cache=None) -> BenchmarkReport:
+    """Generate, build, then time ``runs`` traversals with validation (harness.py:247-296).
+
+    ``csr_cache``: path of a CSR blob (csr.save); reused when its header
+    matches ``params``/``dedup``, otherwise (re)written after the build."""
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}")
     from .engine import resolve_engine
 
     resolve_engine(engine_name)
-    g = csr_mod.generate_graph(params, dedup=dedup)
+    g = _cached_graph(params, dedup, csr_cache)
     seed = params.seed if source_seed is None else source_seed
     sources = sample_sources(g, runs, seed, allow_isolated=allow_isolated)
     rep = run_on_graph(g, sources, mode, heuristic, cfg, validate=True, parent_mode=parent_mode,
                        params=params)
     g.free()
     return rep
+
+
+def _cached_graph(params: GraphParams, dedup: bool, path):
+    import os
+
+    if path is not None and os.path.exists(path):
+        try:
+            rs, adj, m, meta = csr_mod.load_arrays(path)
+            if (meta["scale"], meta["edgefactor"], meta["seed"], meta["probs"], meta["dedup"],
+                    meta["permute_labels"]) == (params.scale, params.edgefactor, params.seed,
+                                                tuple(params.probs), dedup, params.permute_labels):
+                return csr_mod.from_csr(rs, adj, m)
+        except ValueError:
+            pass
+    g = csr_mod.generate_graph(params, dedup=dedup)
+    if path is not None:
+        csr_mod.save(g, path, params=params, dedup=dedup)
+    return g
 
 
 def write_report_csv(report: BenchmarkReport, path) -> None:

@@ -240,3 +240,31 @@ def test_large_graph_kernel_variant_on_small_graphs(cuda, small_golden, golden_h
                 tr = np.array([[x.layer, 1 if x.direction == "bottom-up" else 0, x.v_f, x.e_f, x.e_u,
                                 x.f_value, x.g_value, x.fallback_count, x.gather_count] for x in r.trace])
                 assert np.array_equal(tr, small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)
+
+
+def test_csr_cache_device_roundtrip(cuda, tmp_path):
+    hb = cuda
+    from paper_1704_02259_b200 import csr
+
+    params = hb.GraphParams(scale=12, edgefactor=16, seed=1)
+    g = hb.generate_graph(params)
+    csr.save(g, tmp_path / "g.csr", params=params)
+    g2 = csr.load(tmp_path / "g.csr")
+    assert np.array_equal(g2.row_starts, g.row_starts) and np.array_equal(g2.adjacency, g.adjacency)
+    assert g2.in_edges_total == g.in_edges_total
+    r1 = hb.bfs(g, 5, device=False)
+    r2 = hb.bfs(g2, 5, device=False)
+    assert np.array_equal(r1.parent, r2.parent) and np.array_equal(r1.level, r2.level)
+
+
+def test_run_benchmark_csr_cache(cuda, tmp_path):
+    hb = cuda
+    params = hb.GraphParams(scale=11, edgefactor=8, seed=4)
+    path = tmp_path / "c.csr"
+    r1 = hb.run_benchmark(params, mode="simd-hybrid", runs=4, csr_cache=path)
+    assert path.exists()
+    stamp = path.stat().st_mtime_ns
+    r2 = hb.run_benchmark(params, mode="simd-hybrid", runs=4, csr_cache=path)
+    assert path.stat().st_mtime_ns == stamp  # reused, not rewritten
+    assert [x.source for x in r1.runs] == [x.source for x in r2.runs]
+    assert all(x.valid for x in r1.runs + r2.runs)

@@ -109,3 +109,22 @@ def test_cli_parser():
                                        "beamer", "--dedup", "--alpha", "14", "--beta", "24"])
     assert a.scale == 12 and a.heuristic == "beamer" and a.dedup and a.alpha == 14
     assert a.engine == "cuda" and a.parent_mode == "minid"
+
+
+def test_csr_cache_roundtrip(tmp_path, oracle):
+    from paper_1704_02259_b200 import csr
+
+    u, v = oracle.generate(9, 8, 3)
+    host = oracle.csr_build(u, v, 512)
+    p = hb.GraphParams(scale=9, edgefactor=8, seed=3)
+    path = tmp_path / "g.csr"
+    csr.save(host, path, params=p)
+    rs, adj, m, meta = csr.load_arrays(path)
+    assert np.array_equal(rs, host.row_starts) and np.array_equal(adj, host.adjacency)
+    assert m == len(u) and meta["scale"] == 9 and meta["edgefactor"] == 8 and meta["seed"] == 3
+    assert meta["probs"] == (0.57, 0.19, 0.19, 0.05) and not meta["dedup"]
+    raw = bytearray(path.read_bytes())
+    raw[:8] = b"XXXXXXXX"
+    (tmp_path / "bad.csr").write_bytes(bytes(raw))
+    with pytest.raises(ValueError):
+        csr.load_arrays(tmp_path / "bad.csr")
