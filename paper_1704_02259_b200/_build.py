@@ -20,7 +20,7 @@ LIB = os.path.join(CSRC, "libhbfs.so")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
+FLAGS = [*__import__("shlex").split(__import__("os").environ.get("HBFS_NVCC_EXTRA", "")), "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
 
 
 def sources():

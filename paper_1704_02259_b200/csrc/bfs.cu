@@ -379,7 +379,8 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
             if (hm) {
                 const int j = __ffs(hm) - 1;
                 hit[k] = (int64_t)(base + j);
-                hu[k] = val[j];
+                // select, not val[j]: a dynamic index would put val[] in local memory
+                hu[k] = j == 0 ? val[0] : j == 1 ? val[1] : j == 2 ? val[2] : val[3];
             } else {
                 p[k] = base + 4;
             }
