@@ -223,6 +223,27 @@ __device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
     return (bm[a >> 5] >> (a & 31)) & 1u;
 }
 
+// Bitmap probe through a raw pointer with a 32-bit word index: one wide
+// multiply-add per address instead of a 64-bit add chain.
+__device__ __forceinline__ uint32_t probe_word(const uint32_t *__restrict__ bm, uint32_t a) {
+    return bm[a >> 5];
+}
+
+// Position of the (r+1)-th set bit of m (r < popc(m)); cheaper than __fns.
+__device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t r) {
+    uint32_t pos = 0, c;
+    c = __popc(m & 0xffffu);
+    if (r >= c) { r -= c; m >>= 16; pos += 16; }
+    c = __popc(m & 0xffu);
+    if (r >= c) { r -= c; m >>= 8; pos += 8; }
+    c = __popc(m & 0xfu);
+    if (r >= c) { r -= c; m >>= 4; pos += 4; }
+    c = __popc(m & 0x3u);
+    if (r >= c) { r -= c; m >>= 2; pos += 2; }
+    if (r >= (m & 1u)) pos += 1;
+    return pos;
+}
+
 // Block-aggregated append to a queue: every thread contributes up to I entries
 // (v, deg, row start).  Warps scan their lanes, the CTA scans its warps, and ONE
 // 64-bit atomic per CTA reserves both the queue slots and the arc range
@@ -333,7 +354,8 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // step, lowest position winning (ballot + ffs) — the reference's first-hit rule
 // (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
 template <typename OffT, int K, int LV = kLaneVecs>
-__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const Plane bm,
+__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
+                                           const uint32_t *__restrict__ bm,
                                            const bool (&act)[K], const OffT (&s)[K],
                                            const OffT (&e)[K], int64_t (&hit)[K],
                                            uint32_t (&hu)[K]) {
@@ -364,7 +386,7 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
             for (int j = 0; j < 4; ++j) {
                 const OffT idx = base + j;
                 const bool ok = go[k] && idx >= p[k] && idx < e[k];
-                wd[k][j] = ok ? bm[val[j] >> 5] : 0u;
+                wd[k][j] = ok ? probe_word(bm, val[j]) : 0u;
             }
         }
 #pragma unroll
@@ -406,7 +428,8 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const uint64_t idx = b4 + j;
-                        if (idx >= ps && idx < pe && test_bit(bm, val[j])) hm |= 1u << j;
+                        if (idx >= ps && idx < pe && ((probe_word(bm, val[j]) >> (val[j] & 31)) & 1u))
+                            hm |= 1u << j;
                     }
                 }
                 const unsigned lanes = __ballot_sync(0xffffffffu, hm != 0);
@@ -826,7 +849,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 if (j > 31) j = 31;
                 const uint32_t cm = __shfl_sync(full, candl, j);
                 const uint32_t ex = __shfl_sync(full, incl, j) - __shfl_sync(full, cntl, j);
-                const uint32_t bit = act[k] ? __fns(cm, 0, (int)(c - ex) + 1) : 0u;
+                const uint32_t bit = act[k] ? nth_bit(cm, c - ex) : 0u;
                 v[k] = (uint32_t)((tile * 32 + j) * 32 + bit);
                 s[k] = e[k] = 0;
                 if (act[k]) {
@@ -836,7 +859,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
             int64_t hit[C];
             uint32_t hu[C];
-            first_hits<OffT, C, LV>(A.adj, in, act, s, e, hit, hu);
+            first_hits<OffT, C, LV>(A.adj, in.p, act, s, e, hit, hu);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 if (!act[k]) continue;

@@ -78,11 +78,20 @@ def test_device_generator_and_csr(cuda, small_golden, small_graphs, name):
     assert np.array_equal(hb.sample_sources(g, 8, 1), small_golden[f"{name}/sources"])
 
 
-@pytest.mark.parametrize("defer", [False, True])
+KNOBS = {
+    "plain": {},
+    # deferred level stamping (depth planes + final pass), normally n >= 2^22
+    "defer": {"HBFS_DEFER_LEVELS_MIN_N": "0"},
+    # the large-graph kernel variant (2 searches/lane, scan-tuned bottom-up)
+    "scan_variant": {"HBFS_KERNEL_VARIANT": "3"},
+}
+
+
+@pytest.mark.parametrize("knobs", list(KNOBS))
 @pytest.mark.parametrize("name", SMALL)
-def test_traversals_match_reference(cuda, small_golden, small_graphs, name, defer, monkeypatch):
-    if defer:  # deferred level stamping (depth planes + final pass), normally n >= 2^22
-        monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
+def test_traversals_match_reference(cuda, small_golden, small_graphs, name, knobs, monkeypatch):
+    for k, v in KNOBS[knobs].items():
+        monkeypatch.setenv(k, v)
     hb = cuda
     _, g = small_graphs[name]
     for s in small_golden[f"{name}/sources"]:

@@ -14,6 +14,7 @@ ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--parent-mode", default="minid")
 ap.add_argument("--root", type=int, default=-1)
 ap.add_argument("--phases", action="store_true")
+ap.add_argument("--classes", action="store_true", help="time share per layer class over all roots")
 a = ap.parse_args()
 probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
 t0 = time.time()
@@ -28,10 +29,26 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for s in roots[:2]:
     hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
 tot = []
+cls = {}
+
+
+def layer_class(x):
+    if x.direction == "bottom-up":
+        return "BU dense" if x.v_f * 64 >= n else "BU sparse-frontier"
+    return "TD hub (e_f>=2^21)" if x.e_f >= 1 << 21 else "TD small"
+
+
 for s in roots:
     flush.fill_(1); torch.cuda.synchronize()
     r = hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
     tot.append(r.device_seconds)
+    for x in r.trace:
+        c = cls.setdefault(layer_class(x), [0.0, 0])
+        c[0] += x.elapsed
+        c[1] += 1
+    c = cls.setdefault("fixed (init, levels, launch)", [0.0, 0])
+    c[0] += r.device_seconds - sum(x.elapsed for x in r.trace)
+    c[1] += 1
     if not a.quiet:
         lay = " ".join(f"{"B" if x.direction=="bottom-up" else "T"}{x.v_f}[{x.e_f/1e6:.1f}M]:{x.elapsed*1e6:.1f}us" for x in r.trace)
         print(f"root {int(s)}: {r.device_seconds*1e6:.1f}us  sum(layers)={sum(x.elapsed for x in r.trace)*1e6:.1f}us  {lay}", flush=True)
@@ -55,4 +72,8 @@ for s in roots:
                 marks = [(k, t[k] - t[0]) for k in (1, 2, 3, 4) if t[k]]
                 print(f"   L{i} {x.direction[0].upper()} v_f={x.v_f} e_f={x.e_f}: " + " ".join(f"s{k}@{v/1e3:.1f}us" for k, v in marks))
 m = g.in_edges_total
+if a.classes:
+    T = sum(tot)
+    for k, (t, c) in sorted(cls.items(), key=lambda kv: -kv[1][0]):
+        print(f"  {k:30s} {t/len(tot)*1e6:8.1f} us/root  {100*t/T:5.1f}%  ({c} layers)")
 print(f"hmean GTEPS {len(tot)*m/sum(tot)/1e9:.2f}  mean us {np.mean(tot)*1e6:.1f}")
