@@ -1028,36 +1028,71 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
 // Final level stamp: level[v] = the depth plane holding v (unflushed depths
 // d0..nL-1), -1 if never visited; vertices of flushed depths keep the level
 // written when their plane was recycled.
+// Per-warp staging rows of the level pass: 8 words x 32 levels, rows padded
+// to 36 ints so both the row writes and the column reads are conflict-free.
+constexpr int kLvRow = 36;
+constexpr int kLvStage = 8 * kLvRow;
+
 template <typename OffT>
-__device__ void phase_levels(const Args<OffT> &A, int64_t nL) {
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+__device__ void phase_levels(const Args<OffT> &A, int64_t nL, int32_t *stage) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t d0 = nL + 2 - kPlanes > 0 ? nL + 2 - kPlanes : 0;
-    // thread per word: its depth-plane words (coalesced across the warp), then
-    // its 32 levels as eight 16-byte stores
-    for (int64_t w = tid; w < A.nw; w += nth) {
+    int32_t *st = stage + (threadIdx.x >> 5) * kLvStage;
+    // lane per word: its depth-plane words (coalesced across the warp) are
+    // folded into binary digit words (bit b of D_k = bit k of the depth of
+    // vertex b relative to d0).  The warp's 32 words of levels then go out
+    // through shared memory, 8 words per round, as 512-byte contiguous stores.
+    for (int64_t t = warp; t * 32 < A.nw; t += nwarps) {
+        const int64_t w = t * 32 + lane;
+        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n &&  // warp-uniform
+                          (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
+        if (!fast && w >= A.nw) continue;
         const uint32_t vw = A.bits[w];
-        const bool full_word = (w + 1) * 32 <= A.n;
-        int32_t lv[32];
-#pragma unroll
-        for (int b = 0; b < 32; ++b) lv[b] = ((vw >> b) & 1u) ? -2 : -1;  // -2: visited, flushed
+        uint32_t R = 0, D[5] = {0, 0, 0, 0, 0};
         for (int64_t g0 = d0; g0 < nL; g0 += 8) {
             uint32_t p[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) p[j] = g0 + j < nL ? depth_plane(A, g0 + j)[w] : 0u;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
+                const uint32_t rel = (uint32_t)(g0 + j - d0);
+                R |= p[j];
 #pragma unroll
-                for (int b = 0; b < 32; ++b)
-                    if ((p[j] >> b) & 1u) lv[b] = (int32_t)(g0 + j);
+                for (int k = 0; k < 5; ++k) D[k] |= ((rel >> k) & 1u) ? p[j] : 0u;
             }
         }
-        int32_t *dst = A.level + w * 32;
-        if (full_word && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && d0 == 0) {
+        int32_t lv[32];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                reinterpret_cast<int4 *>(dst)[q] =
-                    make_int4(lv[4 * q], lv[4 * q + 1], lv[4 * q + 2], lv[4 * q + 3]);
+        for (int b = 0; b < 32; ++b) {
+            uint32_t rel = 0;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) rel |= ((D[k] >> b) & 1u) << k;
+            // reached: depth from the planes; visited otherwise: flushed earlier
+            lv[b] = ((R >> b) & 1u) ? (int32_t)(d0 + rel) : (((vw >> b) & 1u) ? -2 : -1);
+        }
+        int32_t *dst = A.level + w * 32;
+        if (fast) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if ((lane >> 3) == r) {
+                    int32_t *row = st + (lane & 7) * kLvRow;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<int4 *>(row)[q] =
+                            make_int4(lv[4 * q], lv[4 * q + 1], lv[4 * q + 2], lv[4 * q + 3]);
+                }
+                __syncwarp();
+                int32_t *gdst = A.level + (t * 32 + 8 * r) * 32;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = h * 4 + (lane >> 3);
+                    const int4 x = *reinterpret_cast<const int4 *>(st + m * kLvRow + (lane & 7) * 4);
+                    reinterpret_cast<int4 *>(gdst + m * 32)[lane & 7] = x;
+                }
+                __syncwarp();
+            }
         } else {
             for (int b = 0; b < 32; ++b)
                 if (w * 32 + b < A.n && lv[b] != -2) dst[b] = lv[b];
@@ -1072,7 +1107,9 @@ __device__ void phase_levels(const Args<OffT> &A, int64_t nL) {
 template <typename OffT, int K, int MINB, bool SCAN>
 __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ TdSmem<OffT> sm;
+    __shared__ TdSmem<OffT> sm;  // also the level pass's staging rows
+    static_assert(sizeof(TdSmem<OffT>) >= (kBlock / 32) * kLvStage * sizeof(int32_t),
+                  "level staging must fit the TD scratch");
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];  // per warp: found bits of its 32-word tile
     __shared__ int64_t s_pre[kCbMaxRanges + 1];
@@ -1208,7 +1245,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     if (S.v_f == 0 && !A.direct_levels) {  // finished in this launch: stamp the levels
         grid.sync();
         if (leader) kstamp[3] = globaltimer();
-        phase_levels(A, S.layer);
+        phase_levels(A, S.layer, reinterpret_cast<int32_t *>(&sm));
         grid.sync();
         if (leader) kstamp[4] = globaltimer();
     }
