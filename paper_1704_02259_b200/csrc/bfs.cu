@@ -585,14 +585,15 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
         if (Harvest) {
             // vis is complete (frontier committed before a barrier) and not
             // written during the expansion: one read-only load per arc, then
-            // the parent update; the harvest pass derives the next frontier
-            // from parent != NIL.
+            // two reductions without return (next-frontier bit, parent); the
+            // harvest pass reads the 1-bit-per-vertex next frontier.
 #pragma unroll
             for (int k = 0; k < I; ++k) vw[k] = ok[k] ? __ldg(&vis[v[k] >> 5]) : ~0u;
 #pragma unroll
             for (int k = 0; k < I; ++k) {
                 const uint32_t b = 1u << (v[k] & 31);
                 if (!(vw[k] & b)) {
+                    atomicOr(&out[v[k] >> 5], b);
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
                 }
@@ -985,11 +986,10 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
     }
 }
 
-// Harvest after a fire-and-forget top-down expansion: a vertex was discovered
-// iff it was unvisited (vis, not written by the expansion) and has a parent
-// now.  Thread per word: parent loads for the word's unvisited non-isolated
-// vertices (one 128-byte line per word), next-frontier word and vis commit,
-// then the found vertices are stamped and appended like phase_convert.
+// Harvest after a fire-and-forget top-down expansion: the next-frontier bits
+// were set by reductions (a vertex was discovered iff it was unvisited before
+// the layer and some frontier arc reached it).  Thread per word: vis commit,
+// count and degree sum of the found vertices (and their levels on small graphs).
 template <typename OffT>
 __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
                               unsigned long long *red, int32_t depth1) {
@@ -998,17 +998,9 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
     for (int64_t w = tid; w < A.nw; w += nth) {
-        const uint32_t vw = vis[w];
-        uint32_t un = ~vw & __ldg(A.posw + w), bits = 0;
-        const uint32_t *pw = A.parent + w * 32;
-        while (un) {
-            const int b = __ffs(un) - 1;
-            un &= un - 1;
-            if (pw[b] != HBFS_NIL) bits |= 1u << b;
-        }
-        out[w] = bits;
+        const uint32_t bits = __ldcg(&out[w]);  // set by the expansion's reductions
         if (bits) {
-            vis[w] = vw | bits;
+            vis[w] |= bits;
             acc += ((unsigned long long)__popc(bits) << kPackShift) + word_degsum(A, w, bits);
             if (A.direct_levels)
                 for (uint32_t x = bits; x; x &= x - 1) A.level[w * 32 + __ffs(x) - 1] = depth1;

@@ -207,6 +207,11 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
                     r = hb.bfs(g, s, device=False, **kw)
                     assert np.array_equal(r.level, small_golden[f"{name}/{s}/level"]), (name, s, mode)
                     assert np.array_equal(r.parent, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
+                    # the harvest's counters (next v_f, e_f) drive the trace
+                    tr = np.array([[x.layer, 1 if x.direction == "bottom-up" else 0, x.v_f, x.e_f, x.e_u,
+                                    x.f_value, x.g_value, x.fallback_count, x.gather_count]
+                                   for x in r.trace])
+                    assert np.array_equal(tr, small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)
                 ra = hb.bfs(g, s, device=False, parent_mode="any", force_direction="top-down")
                 assert np.array_equal(ra.level, small_golden[f"{name}/{s}/level"])
                 assert hb.validate_tree(g, s, ra.parent, ra.level).ok
@@ -219,8 +224,8 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
 
 
 def test_large_graph_kernel_variant_on_small_graphs(cuda, small_golden, golden_hashes, monkeypatch):
-    """The SCALE>=24 kernel variant (2 CTAs/SM, tiny-frontier scan path with the
-    shared-memory frontier summary) forced on the golden small graphs."""
+    """The SCALE>=24 kernel variant (2 CTAs/SM, 4-vector bottom-up probes on
+    tiny-frontier layers) forced on the golden small graphs."""
     hb = cuda
     monkeypatch.setenv("HBFS_KERNEL_VARIANT", "3")
     for meta in golden_hashes["small"]:
