@@ -772,28 +772,18 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
 // those of the reference's 16-lane kernel.  Replaces
 // bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
 // bu_probe.h:22-106).
-// Warp tile scheduler: a static share first (tiles warp + k*nwarps, k < kGrab:
-// no atomics, short layers spread over all warps), then dynamic grabs of kGrab
-// consecutive tiles from a per-layer counter (balances long layers).
+// Warp tile scheduler: the first tile is the warp's own index (no atomic, so
+// short layers spread over all warps), then one tile per atomic grab from a
+// per-layer counter (balances long layers).
 struct TileSched {
-    static constexpr int64_t kGrab = 1;
     unsigned long long *work;
-    int64_t tile, nwarps, k = 0, dyn_end = -1;
+    int64_t tile, nwarps;
     __device__ TileSched(unsigned long long *w, int64_t warp, int64_t nw)
         : work(w), tile(warp), nwarps(nw) {}
     __device__ __forceinline__ int64_t next() {
-        if (dyn_end < 0) {
-            if (++k < kGrab) tile += nwarps;
-            else dyn_end = 0;
-        } else {
-            ++tile;
-        }
-        if (dyn_end >= 0 && tile >= dyn_end) {
-            unsigned long long t = 0;
-            if ((threadIdx.x & 31) == 0) t = atomicAdd(work, (unsigned long long)kGrab);
-            tile = nwarps * kGrab + (int64_t)__shfl_sync(0xffffffffu, t, 0);
-            dyn_end = tile + kGrab;
-        }
+        unsigned long long t = 0;
+        if ((threadIdx.x & 31) == 0) t = atomicAdd(work, 1ull);
+        tile = nwarps + (int64_t)__shfl_sync(0xffffffffu, t, 0);
         return tile;
     }
 };
@@ -908,19 +898,15 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     __syncthreads();
 }
 
-// Word-level append: thread t contributes the vertices of bitmap word w (bits),
-// whose count and degree sum it computed; one CTA scan + one atomic reserves
-// the queue slots and arc range of all 512 words, then every thread writes its
-// entries (vertex, arc offset, row start) and the chunk starts inside its arc
-// range in order.  Optionally stamps level = stamp.  Block-uniform call.
-template <typename OffT>
-__device__ __forceinline__ void word_enqueue(const Args<OffT> &A, const Queue<OffT> &Q, int64_t w,
-                                             uint32_t bits, uint32_t cnt, uint64_t dsum,
-                                             unsigned long long *counter, int32_t stamp,
-                                             EnqSmem &es) {
+// Block-wide reservation: each thread brings x = count<<35 | degree sum; one
+// CTA scan + one atomic on `counter` reserves the queue slots and arc range of
+// the whole block; returns the thread's (exclusive) packed base.  Block-uniform.
+__device__ __forceinline__ unsigned long long block_reserve(unsigned long long mine,
+                                                            unsigned long long *counter,
+                                                            EnqSmem &es) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long x = ((unsigned long long)cnt << kPackShift) + dsum;  // packed, inclusive scan
+    unsigned long long x = mine;  // inclusive warp scan
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(full, x, o);
@@ -938,9 +924,16 @@ __device__ __forceinline__ void word_enqueue(const Args<OffT> &A, const Queue<Of
         es.wbase[0] = run ? atomicAdd(counter, run) : 0ull;
     }
     __syncthreads();
-    if (!cnt) return;
-    const unsigned long long mine = ((unsigned long long)cnt << kPackShift) + dsum;
-    const unsigned long long base = es.wbase[0] + es.wtot[wid] + (x - mine);
+    return es.wbase[0] + es.wtot[wid] + (x - mine);
+}
+
+// Append the vertices of bitmap word w (bits) at packed position `base`
+// (queue slot << 35 | arc offset): vertex, arc offset, row start, and the
+// chunk starts inside its arc range; returns the advanced position.
+template <typename OffT>
+__device__ __forceinline__ unsigned long long word_append(const Args<OffT> &A, const Queue<OffT> &Q,
+                                                          int64_t w, uint32_t bits,
+                                                          unsigned long long base) {
     uint64_t pos = base >> kPackShift, off = base & kPackMask;
     while (bits) {
         const uint32_t v = (uint32_t)(w * 32 + __ffs(bits) - 1);
@@ -955,6 +948,7 @@ __device__ __forceinline__ void word_enqueue(const Args<OffT> &A, const Queue<Of
         ++pos;
         off += d;
     }
+    return ((unsigned long long)pos << kPackShift) | off;
 }
 
 // degree sum of the vertices of word w in `bits`
@@ -970,19 +964,39 @@ __device__ __forceinline__ uint64_t word_degsum(const Args<OffT> &A, int64_t w, 
 }
 
 // Bitmap -> queue (with arc prefix, row starts, chunk starts) at a bottom-up ->
-// top-down switch: thread per frontier word, word_enqueue per 512 words.
+// top-down switch: each thread takes up to kConvWords consecutive words (fewer
+// on small graphs, to keep every CTA busy), so a block round covers up to 2048
+// words with one reservation; rounds without any frontier bit cost one barrier.
+constexpr int kConvWords = 4;
 
 template <typename OffT>
 __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const Plane bm,
-                              unsigned long long *counter, int32_t stamp_level, bool commit_vis,
-                              EnqSmem &es) {
+                              unsigned long long *counter, bool commit_vis, EnqSmem &es) {
     const Plane vis{A.bits};
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < A.nw; w0 += stride) {
-        const int64_t w = w0 + threadIdx.x;
-        const uint32_t bits = w < A.nw ? bm[w] : 0u;
-        if (commit_vis && bits) vis[w] |= bits;
-        word_enqueue(A, Q, w, bits, __popc(bits), word_degsum(A, w, bits), counter, stamp_level, es);
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int wpt = A.nw >= kConvWords * nth ? kConvWords : (int)(A.nw / nth > 1 ? A.nw / nth : 1);
+    const int64_t span = (int64_t)blockDim.x * wpt;
+    for (int64_t b0 = (int64_t)blockIdx.x * span; b0 < A.nw; b0 += (int64_t)gridDim.x * span) {
+        const int64_t w0 = b0 + (int64_t)threadIdx.x * wpt;
+        uint32_t bits[kConvWords];
+#pragma unroll
+        for (int i = 0; i < kConvWords; ++i) bits[i] = i < wpt && w0 + i < A.nw ? bm[w0 + i] : 0u;
+        uint32_t cnt = 0;
+        uint64_t dsum = 0;
+#pragma unroll
+        for (int i = 0; i < kConvWords; ++i) {
+            if (!bits[i]) continue;
+            if (commit_vis) vis[w0 + i] |= bits[i];
+            cnt += __popc(bits[i]);
+            dsum += word_degsum(A, w0 + i, bits[i]);
+        }
+        if (!__syncthreads_or(cnt != 0)) continue;
+        unsigned long long base =
+            block_reserve(((unsigned long long)cnt << kPackShift) + dsum, counter, es);
+        if (!cnt) continue;
+#pragma unroll
+        for (int i = 0; i < kConvWords; ++i)
+            if (bits[i]) base = word_append(A, Q, w0 + i, bits[i], base);
     }
 }
 
@@ -1150,7 +1164,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                     spare = depth_plane(A, L + 2);
         Ctr *ctr = &A.ctl->ctr[L % 3];
         if (dir == HBFS_TOP_DOWN && S.kind == 1) {
-            phase_convert(A, A.qb[L & 1], in, &A.ctl->conv, 0, false, sm.enq);
+            phase_convert(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
             grid.sync();
             STAMP(1);
         }
