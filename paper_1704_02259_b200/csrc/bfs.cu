@@ -45,6 +45,11 @@ constexpr int kTdChunk = kBlock * kTdItems;  // arcs per CTA work item
 // bottom-up layers whose frontier is tiny (most rows are scanned to the end)
 constexpr int kLaneVecs = 2;
 constexpr int kLaneVecsScan = 4;
+// Single first probe when the frontier holds >= n/16 vertices — on graphs
+// without hubs (max degree < 64x the mean, e.g. uniform): there it saves
+// probe traffic (uniform 2^22: +7%); on Kronecker graphs the extra dependent
+// step costs more than the saved probes (SCALE 20: -6%).
+constexpr int64_t kFirst1Div = 16;
 constexpr int kPackShift = 35;               // packed counter: count<<35 | degree sum
 constexpr unsigned long long kPackMask = (1ull << kPackShift) - 1;
 constexpr int64_t kRowsCap = 1024;           // trace rows per launch
@@ -136,6 +141,7 @@ struct Args {
     Heur H;
     int max_pos, use_simd, parent_mode, do_init;
     int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
+    int64_t first1_div;  // bottom-up probes a row's first entry alone when v_f >= n / first1_div
     uint32_t root;
 };
 
@@ -353,7 +359,10 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // kLaneVecs vectors are finished by a warp-cooperative scan, 128 entries per
 // step, lowest position winning (ballot + ffs) — the reference's first-hit rule
 // (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
-template <typename OffT, int K, int LV = kLaneVecs>
+// FIRST1 (dense frontiers, where nearly every found vertex hits at its first
+// entry): probe that entry alone before the vectors — one bitmap load instead
+// of up to four.
+template <typename OffT, int K, int LV, bool FIRST1>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                                            const uint32_t *__restrict__ bm,
                                            const bool (&act)[K], const OffT (&s)[K],
@@ -366,6 +375,23 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
         p[k] = s[k];
         hit[k] = -1;
         hu[k] = 0;
+    }
+    if (FIRST1) {
+        uint32_t a[K], wd[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) a[k] = act[k] && p[k] < e[k] ? __ldg(adj + p[k]) : 0u;
+#pragma unroll
+        for (int k = 0; k < K; ++k) wd[k] = act[k] && p[k] < e[k] ? probe_word(bm, a[k]) : 0u;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!act[k] || p[k] >= e[k]) continue;
+            if ((wd[k] >> (a[k] & 31)) & 1u) {
+                hit[k] = (int64_t)p[k];
+                hu[k] = a[k];
+            } else {
+                ++p[k];
+            }
+        }
     }
 #pragma unroll
     for (int it = 0; it < LV; ++it) {
@@ -788,7 +814,7 @@ struct TileSched {
     }
 };
 
-template <typename OffT, int C, int LV>
+template <typename OffT, int C, int LV, bool FIRST1>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
@@ -850,7 +876,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
             int64_t hit[C];
             uint32_t hu[C];
-            first_hits<OffT, C, LV>(A.adj, in.p, act, s, e, hit, hu);
+            first_hits<OffT, C, LV, FIRST1>(A.adj, in.p, act, s, e, hit, hu);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 if (!act[k]) continue;
@@ -1204,8 +1230,10 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
             if (SCAN && S.v_f * 64 < A.n)
-                phase_bu<OffT, K, kLaneVecsScan>(A, S, in, out, spare, ctr, red, sf);
-            else phase_bu<OffT, K, kLaneVecs>(A, S, in, out, spare, ctr, red, sf);
+                phase_bu<OffT, K, kLaneVecsScan, false>(A, S, in, out, spare, ctr, red, sf);
+            else if (S.v_f * A.first1_div >= A.n)
+                phase_bu<OffT, K, kLaneVecs, true>(A, S, in, out, spare, ctr, red, sf);
+            else phase_bu<OffT, K, kLaneVecs, false>(A, S, in, out, spare, ctr, red, sf);
         }
         grid.sync();
 
@@ -1413,6 +1441,8 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     // level arrays that fit L2 take scattered stores cheaply; larger graphs
     // stamp levels once from the depth planes (HBFS_DEFER_LEVELS_MIN_N: test knob)
     A.direct_levels = g->n < env_i64("HBFS_DEFER_LEVELS_MIN_N", int64_t(1) << 22);
+    const bool hubless = g->n > 0 && g->max_degree * g->n < 64 * g->arcs;
+    A.first1_div = env_i64("HBFS_FIRST1_DIV", hubless ? kFirst1Div : 0);  // knob; 0 = never
     A.cbq.q = w->cbq.as<uint32_t>();
     A.cbq.qo = w->cbqo.as<OffT>();
     A.cbq.qr = w->cbqr.as<OffT>();

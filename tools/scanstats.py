@@ -36,6 +36,15 @@ for c0 in range(0, adj.numel(), CH):
 found = cand & (first < (1 << 40))
 scan = torch.where(found, first + 1, deg)[cand]
 print(f"found {int(found.sum())}  entries probed (to first hit or row end) {int(scan.sum())}")
+fp = first[found]
+tot = float(found.sum())
+print("first-hit position among found: " + ", ".join(
+    f"{k}: {100 * float((fp == k).sum()) / tot:.1f}%" for k in range(4)) +
+      f", >=4: {100 * float((fp >= 4).sum()) / tot:.1f}%")
+# probes issued by the current lane phase: whole aligned vectors until the hit / row end
+off_all = (rs[:-1] & 3)
+vec_probes = torch.minimum(((off_all + torch.where(found, first + 1, deg) + 3) // 4) * 4 - off_all, deg)[cand]
+print(f"probes with 4-entry vectors {int(vec_probes.sum())}  vs exact {int(scan.sum())}")
 # lane phase covers the aligned vectors starting at rs & ~3: entries up to LE - (rs & 3)
 off = (rs[:-1] & 3)[cand]
 lane_cov = (a.lane_entries - off).clamp(min=0)
