@@ -45,6 +45,7 @@ constexpr int kTdChunk = kBlock * kTdItems;  // arcs per CTA work item
 // bottom-up layers whose frontier is tiny (most rows are scanned to the end)
 constexpr int kLaneVecs = 2;
 constexpr int kLaneVecsScan = 4;
+constexpr uint64_t kTailLong = 256;  // open rows longer than this use the whole-warp scan
 // Single first probe when the frontier holds >= n/16 vertices — on graphs
 // without hubs (max degree < 64x the mean, e.g. uniform): there it saves
 // probe traffic (uniform 2^22: +7%); on Kronecker graphs the extra dependent
@@ -434,14 +435,72 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
             }
         }
     }
+    // Rows still open: short ones four at a time (8 lanes x 4 entries per row
+    // per step, lowest position in each 8-lane group wins), rows with more than
+    // kTailLong entries left by the whole warp (128 entries per step).
+    const unsigned full = 0xffffffffu;
+    const int grp = lane >> 3, gl = lane & 7;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        unsigned todo = __ballot_sync(0xffffffffu, act[k] && hit[k] < 0 && p[k] < e[k]);
+        const bool open = act[k] && hit[k] < 0 && p[k] < e[k];
+        unsigned todo_long = __ballot_sync(full, open && (uint64_t)(e[k] - p[k]) > kTailLong);
+        unsigned todo = __ballot_sync(full, open) & ~todo_long;
         while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint64_t ps = __shfl_sync(0xffffffffu, (unsigned long long)p[k], src);
-            const uint64_t pe = __shfl_sync(0xffffffffu, (unsigned long long)e[k], src);
+            unsigned t = todo;
+            for (int g = 0; g < grp && t; ++g) t &= t - 1;  // group g takes the g-th open row
+            const int src = t ? __ffs(t) - 1 : -1;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) todo &= todo - 1;
+            const int sl = src < 0 ? 0 : src;
+            const OffT ps = __shfl_sync(full, p[k], sl), pe = __shfl_sync(full, e[k], sl);
+            bool live = src >= 0;
+            int64_t h = -1;
+            uint32_t hv = 0;
+            for (OffT c = ps & ~(OffT)3;; c += 32) {
+                live = live && c < pe;
+                if (!__any_sync(full, live)) break;
+                const OffT b4 = c + 4 * gl;
+                uint32_t hm = 0;
+                uint4 q4 = make_uint4(0, 0, 0, 0);
+                if (live && b4 < pe) {
+                    q4 = __ldg(reinterpret_cast<const uint4 *>(adj + b4));
+                    const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const OffT idx = b4 + j;
+                        if (idx >= ps && idx < pe && ((probe_word(bm, val[j]) >> (val[j] & 31)) & 1u))
+                            hm |= 1u << j;
+                    }
+                }
+                const unsigned gm = (__ballot_sync(full, hm != 0) >> (grp * 8)) & 0xffu;
+                const int jm = hm ? __ffs(hm) - 1 : 0;
+                const uint32_t mine = jm == 0 ? q4.x : jm == 1 ? q4.y : jm == 2 ? q4.z : q4.w;
+                const int wl = gm ? __ffs(gm) - 1 : 0;
+                const int srcl = grp * 8 + wl;
+                const int jw = __shfl_sync(full, jm, srcl);
+                const uint32_t vw = __shfl_sync(full, mine, srcl);
+                if (live && gm) {
+                    h = (int64_t)(c + 4 * wl + jw);
+                    hv = vw;
+                    live = false;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {  // results back to the rows' owners
+                const int og = __shfl_sync(full, src, g * 8);
+                const int64_t hg = __shfl_sync(full, (long long)h, g * 8);
+                const uint32_t vg = __shfl_sync(full, hv, g * 8);
+                if (lane == og) {
+                    hit[k] = hg;
+                    hu[k] = vg;
+                }
+            }
+        }
+        while (todo_long) {
+            const int src = __ffs(todo_long) - 1;
+            todo_long &= todo_long - 1;
+            const uint64_t ps = __shfl_sync(full, (unsigned long long)p[k], src);
+            const uint64_t pe = __shfl_sync(full, (unsigned long long)e[k], src);
             int64_t h = -1;
             uint32_t hv = 0;
             for (uint64_t c = ps & ~3ull; c < pe; c += 128) {
@@ -458,17 +517,12 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                             hm |= 1u << j;
                     }
                 }
-                const unsigned lanes = __ballot_sync(0xffffffffu, hm != 0);
+                const unsigned lanes = __ballot_sync(full, hm != 0);
                 if (lanes) {
                     const int l = __ffs(lanes) - 1;
-                    const uint32_t hml = __shfl_sync(0xffffffffu, hm, l);
-                    const int j = __ffs(hml) - 1;
-                    const uint32_t vals[4] = {q4.x, q4.y, q4.z, q4.w};
-                    uint32_t mine = 0;
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        if (jj == j) mine = vals[jj];
-                    hv = __shfl_sync(0xffffffffu, mine, l);
+                    const int j = __ffs(__shfl_sync(full, hm, l)) - 1;
+                    const uint32_t mine = j == 0 ? q4.x : j == 1 ? q4.y : j == 2 ? q4.z : q4.w;
+                    hv = __shfl_sync(full, mine, l);
                     h = (int64_t)(c + 4 * l + j);
                     break;
                 }

@@ -275,7 +275,7 @@ static int build_from_edges_dev(const uint32_t *du, const uint32_t *dv, int64_t 
         g->n = n;
         g->arcs = arcs;
         g->m_edges = m;
-        g->wide = arcs >= (int64_t(1) << 32);
+        g->wide = arcs >= (int64_t(1) << 32) - 1024;  // 32-bit offsets keep 1024 of headroom
         HB_CHECK(alloc_adj(g));
         k_key_to_adj<<<grid_for(arcs), 256, 0, st>>>(arcs, sb, sorted, g->adj.as<uint32_t>());
         HB_CUDA(cudaGetLastError());
@@ -347,7 +347,7 @@ extern "C" int hbfs_graph_from_csr(const int64_t *row_starts, const uint32_t *ad
     g->n = n;
     g->arcs = arcs;
     g->m_edges = m_edges;
-    g->wide = arcs >= (int64_t(1) << 32);
+    g->wide = arcs >= (int64_t(1) << 32) - 1024;  // 32-bit offsets keep 1024 of headroom
     int rc = alloc_adj(g);
     DevBuf rs64;
     if (!rc) rc = rs64.alloc((n + 1) * 8);
