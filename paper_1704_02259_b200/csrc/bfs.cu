@@ -363,12 +363,22 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // FIRST1 (dense frontiers, where nearly every found vertex hits at its first
 // entry): probe that entry alone before the vectors — one bitmap load instead
 // of up to four.
+// Opaque copy of a pointer: the compiler cannot rematerialise it (it would
+// otherwise rebuild the bitmap plane address from the parameter bank with a
+// 64-bit add chain at every probe — 5 extra instructions per probe).
+__device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
+    const uint32_t *q;
+    asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+    return q;
+}
+
 template <typename OffT, int K, int LV, bool FIRST1>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
-                                           const uint32_t *__restrict__ bm,
+                                           const uint32_t *__restrict__ bm_in,
                                            const bool (&act)[K], const OffT (&s)[K],
                                            const OffT (&e)[K], int64_t (&hit)[K],
                                            uint32_t (&hu)[K]) {
+    const uint32_t *__restrict__ bm = pin_ptr(bm_in);
     const int lane = threadIdx.x & 31;
     OffT p[K];
 #pragma unroll
