@@ -300,51 +300,35 @@ __device__ __forceinline__ void block_enqueue(const bool (&claim)[I], const uint
     if (wtot == 0) return;
     const unsigned long long base = es.wbase[0] + es.wtot[wid];
     const uint64_t qb = base >> kPackShift, db = base & kPackMask;
-    const uint64_t totd = wtot & kPackMask;
-    {
-        uint64_t pos = qb + ci - cl, off = db + di - dl;
+    // Queue entries, then the chunk starts inside each entry's arc range
+    // (chunk c starts at arc c*kTdChunk): an entry spanning at most two chunk
+    // boundaries writes them itself, larger ones (hubs) are written by the
+    // whole warp, 32 per step.
+    uint64_t pos = qb + ci - cl, off = db + di - dl;
 #pragma unroll
-        for (int k = 0; k < I; ++k) {
-            if (claim[k]) {
-                Q.q[pos] = v[k];
-                Q.qo[pos] = (OffT)off;
-                Q.qr[pos] = rsv[k];
-                ++pos;
-                off += deg[k];
-            }
+    for (int k = 0; k < I; ++k) {
+        uint64_t c0 = 0, c1 = 0;
+        const uint64_t mypos = pos;
+        if (claim[k]) {
+            Q.q[pos] = v[k];
+            Q.qo[pos] = (OffT)off;
+            Q.qr[pos] = rsv[k];
+            c0 = (off + kTdChunk - 1) / kTdChunk;
+            c1 = (off + deg[k] + kTdChunk - 1) / kTdChunk;
+            if (c1 - c0 <= 2)
+                for (uint64_t c = c0; c < c1; ++c) Q.cs[c] = (uint32_t)pos;
+            ++pos;
+            off += deg[k];
         }
-    }
-    if (totd == 0) return;
-    const uint64_t c_lo = (db + kTdChunk - 1) / kTdChunk;
-    const uint64_t c_hi = (db + totd - 1) / kTdChunk;
-    for (uint64_t c0 = c_lo; c0 <= c_hi; c0 += 32) {
-        const uint64_t c = c0 + lane;
-        const uint64_t t = c * kTdChunk - db;  // arc offset inside the warp's range
-        int l = 0;                              // lane whose range holds t
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const uint64_t val = __shfl_sync(full, di, l + step - 1);
-            if (val <= t) l += step;
+        unsigned todo = __ballot_sync(full, c1 - c0 > 2);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint64_t b0 = __shfl_sync(full, (unsigned long long)c0, src);
+            const uint64_t b1 = __shfl_sync(full, (unsigned long long)c1, src);
+            const uint32_t bp = (uint32_t)__shfl_sync(full, (unsigned long long)mypos, src);
+            for (uint64_t c = b0 + lane; c < b1; c += 32) Q.cs[c] = bp;
         }
-        if (l > 31) l = 31;
-        const uint64_t rel = t - (__shfl_sync(full, di, l) - __shfl_sync(full, dl, l));
-        uint32_t idx = 0;
-        uint64_t acc = 0;
-        bool found = false;
-#pragma unroll
-        for (int k = 0; k < I; ++k) {
-            const uint64_t dk = __shfl_sync(full, claim[k] ? deg[k] : 0ull, l);
-            const bool ck = __shfl_sync(full, claim[k] ? 1 : 0, l) != 0;
-            if (!found && ck) {
-                if (rel < acc + dk) found = true;
-                else {
-                    acc += dk;
-                    ++idx;
-                }
-            }
-        }
-        const uint64_t qpos = qb + (__shfl_sync(full, ci, l) - __shfl_sync(full, cl, l)) + idx;
-        if (c <= c_hi) Q.cs[c] = (uint32_t)qpos;
     }
 }
 
@@ -352,6 +336,15 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
     return x;
+}
+
+// Opaque copy of a pointer: the compiler cannot rematerialise it (it would
+// otherwise rebuild the bitmap plane address from the parameter bank with a
+// 64-bit add chain at every probe — 5 extra instructions per probe).
+__device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
+    const uint32_t *q;
+    asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+    return q;
 }
 
 // First hit search.  Lane-parallel: for each k, an active lane searches its own
@@ -363,15 +356,6 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 // FIRST1 (dense frontiers, where nearly every found vertex hits at its first
 // entry): probe that entry alone before the vectors — one bitmap load instead
 // of up to four.
-// Opaque copy of a pointer: the compiler cannot rematerialise it (it would
-// otherwise rebuild the bitmap plane address from the parameter bank with a
-// 64-bit add chain at every probe — 5 extra instructions per probe).
-__device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
-    const uint32_t *q;
-    asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
-    return q;
-}
-
 template <typename OffT, int K, int LV, bool FIRST1>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                                            const uint32_t *__restrict__ bm_in,

@@ -69,7 +69,7 @@ for s in roots:
             for i, x in enumerate(r.trace):
                 t = buf[i * 8:(i + 1) * 8].astype(np.int64)
                 print(f"     B_sector {pl[i]/1e6:.1f} MB -> {pl[i]/max(x.elapsed,1e-9)/1e9:.0f} GB/s", end="")
-                marks = [(k, t[k] - t[0]) for k in (1, 2, 3, 4) if t[k]]
+                marks = [(k, t[k] - t[0]) for k in (1, 2, 3, 5, 7, 6, 4) if t[k]]
                 print(f"   L{i} {x.direction[0].upper()} v_f={x.v_f} e_f={x.e_f}: " + " ".join(f"s{k}@{v/1e3:.1f}us" for k, v in marks))
 m = g.in_edges_total
 if a.classes:
