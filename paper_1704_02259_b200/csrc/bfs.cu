@@ -45,6 +45,7 @@ constexpr int kTdChunk = kBlock * kTdItems;  // arcs per CTA work item
 // bottom-up layers whose frontier is tiny (most rows are scanned to the end)
 constexpr int kLaneVecs = 2;
 constexpr int kLaneVecsScan = 4;
+constexpr int kTdMaxSub = 8;  // top-down chunk split on small layers (2048 / 8 = 256 arcs per CTA)
 constexpr uint64_t kTailLong = 256;  // open rows longer than this use the whole-warp scan
 // Single first probe when the frontier holds >= n/16 vertices — on graphs
 // without hubs (max degree < 64x the mean, e.g. uniform): there it saves
@@ -604,16 +605,19 @@ __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare)
 // RED.MIN (min-id) or a plain store (any) on its parent; levels, counters and
 // the next queue come from a word-order harvest of the bitmap afterwards.
 // SPAN: base chunks (of kTdChunk arcs) per work item; harvest layers use 2.
+// Small layers split a chunk into `nsub` sub-items (part `sub`) so that more
+// CTAs share it: a single SM's request rate, not latency, bounds a lone chunk.
 template <typename OffT, bool Harvest, int SPAN>
 __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
                                          uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
                                          const Plane in, const Plane out, const Queue<OffT> &NQ,
-                                         Ctr *ctr, TdSmem<OffT> &sm) {
+                                         Ctr *ctr, TdSmem<OffT> &sm, int sub = 0, int nsub = 1) {
     constexpr int I = kTdItems * SPAN;
     const Plane vis{A.bits};
     const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
-        const uint64_t a0 = (uint64_t)c * kTdChunk;
-        const uint64_t a1 = min(a0 + (uint64_t)kTdChunk * SPAN, mf);
+        const uint64_t span = (uint64_t)kTdChunk * SPAN / nsub;
+        const uint64_t a0 = (uint64_t)c * kTdChunk + (uint64_t)sub * span;
+        const uint64_t a1 = min(a0 + span, mf);
         if (threadIdx.x == 0) {
             const int64_t q0 = Q.cs[c];
             const int64_t ql = (c + SPAN < nchunks) ? (int64_t)Q.cs[c + SPAN] : nf - 1;
@@ -739,9 +743,12 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t nchunks = (int64_t)((mf + kTdChunk - 1) / kTdChunk);
     const int64_t nitems = (nchunks + SPAN - 1) / SPAN;
     unsigned long long *work = &A.ctl->work[S.layer % 3];
-    for (int64_t g = blockIdx.x; g < nitems; g = block_grab(work, &sm.item))
-        td_chunk<OffT, Harvest, SPAN>(A, Q, nf, mf, g * SPAN, nchunks, (int32_t)S.layer + 1, in, out,
-                                      NQ, ctr, sm);
+    int nsub = 1;  // sub-items per chunk on layers with fewer chunks than half the CTAs
+    if (!Harvest)
+        while (nsub < kTdMaxSub && nitems * nsub * 4 <= (int64_t)gridDim.x) nsub *= 2;
+    for (int64_t g = blockIdx.x; g < nitems * nsub; g = block_grab(work, &sm.item))
+        td_chunk<OffT, Harvest, SPAN>(A, Q, nf, mf, (g / nsub) * SPAN, nchunks, (int32_t)S.layer + 1, in,
+                                      out, NQ, ctr, sm, (int)(g % nsub), nsub);
 }
 
 template <typename OffT>

@@ -15,6 +15,8 @@ ap.add_argument("--parent-mode", default="minid")
 ap.add_argument("--root", type=int, default=-1)
 ap.add_argument("--phases", action="store_true")
 ap.add_argument("--classes", action="store_true", help="time share per layer class over all roots")
+ap.add_argument("--flush", default="write", choices=("write", "read", "none"),
+                help="L2 flush before each traversal: write a 256 MB buffer (bench.py's), read it, or none")
 a = ap.parse_args()
 probs = (0.25,) * 4 if a.uniform else (0.57, 0.19, 0.19, 0.05)
 t0 = time.time()
@@ -39,7 +41,11 @@ def layer_class(x):
 
 
 for s in roots:
-    flush.fill_(1); torch.cuda.synchronize()
+    if a.flush == "write":
+        flush.fill_(1)
+    elif a.flush == "read":
+        flush.sum(dtype=torch.int64)
+    torch.cuda.synchronize()
     r = hb.bfs(g, int(s), p, device=True, out=(par, lev), parent_mode=a.parent_mode)
     tot.append(r.device_seconds)
     for x in r.trace:
