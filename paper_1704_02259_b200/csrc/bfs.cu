@@ -82,7 +82,8 @@ struct Ctr {
 // persists it here so a traversal can resume across launches.
 struct Ctl {
     int64_t layer, v_f, e_f, eu_v, eu_e, prev_vf;
-    int32_t dir, kind, done, pad0;
+    int32_t dir, kind, done;
+    uint32_t lv_done;           // CTAs finished in the level kernel (diagnostics)
     int64_t rows;               // rows written by the last launch
     unsigned long long conv;    // enqueue counter of the bitmap->queue phase
     Ctr ctr[3];
@@ -564,6 +565,7 @@ __device__ void phase_init(const Args<OffT> &A) {
             for (int r = 0; r < kCbMaxRanges; ++r) c->cbctr[b][r] = 0;
         c->conv = 0;
         c->done = 0;
+        c->lv_done = 0;
     }
 }
 
@@ -1114,75 +1116,92 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
 
 // Final level stamp: level[v] = the depth plane holding v (unflushed depths
 // d0..nL-1), -1 if never visited; vertices of flushed depths keep the level
-// written when their plane was recycled.
-// Per-warp staging rows of the level pass: 8 words x 32 levels, rows padded
-// to 36 ints so both the row writes and the column reads are conflict-free.
-constexpr int kLvRow = 36;
-constexpr int kLvStage = 8 * kLvRow;
+// written when their plane was recycled.  A separate kernel launched right
+// after the traversal (same stream): it needs the registers the persistent
+// kernel cannot spare (all of a word's planes in flight at once) and a plain
+// grid with one 32-word tile per warp, so every load of the pass is issued
+// up front.  It reads the layer count from the persisted controller state and
+// does nothing unless the traversal finished.
+constexpr int kLvBlock = 256;
+constexpr int kLvBatch = 16;
+
+__device__ __forceinline__ int32_t level_of(uint32_t R, const uint32_t (&D)[5], uint32_t vw,
+                                            int64_t d0, int b) {
+    uint32_t rel = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) rel |= ((D[k] >> b) & 1u) << k;
+    // reached: depth from the planes; visited otherwise: flushed earlier
+    return ((R >> b) & 1u) ? (int32_t)(d0 + rel) : (((vw >> b) & 1u) ? -2 : -1);
+}
 
 template <typename OffT>
-__device__ void phase_levels(const Args<OffT> &A, int64_t nL, int32_t *stage) {
+__global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
+    const Ctl *c = A.ctl;
+    if (!__ldcg(&c->done)) return;
+    unsigned long long *kstamp = A.phase_ns + kRowsCap * kPhaseSlots;
+    if (blockIdx.x == 0 && threadIdx.x == 0) kstamp[3] = globaltimer();
+    const int64_t nL = __ldcg(&c->layer);
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // tile
     const int64_t d0 = nL + 2 - kPlanes > 0 ? nL + 2 - kPlanes : 0;
-    int32_t *st = stage + (threadIdx.x >> 5) * kLvStage;
-    // lane per word: its depth-plane words (coalesced across the warp) are
-    // folded into binary digit words (bit b of D_k = bit k of the depth of
-    // vertex b relative to d0).  The warp's 32 words of levels then go out
-    // through shared memory, 8 words per round, as 512-byte contiguous stores.
-    for (int64_t t = warp; t * 32 < A.nw; t += nwarps) {
-        const int64_t w = t * 32 + lane;
-        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n &&  // warp-uniform
-                          (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
-        if (!fast && w >= A.nw) continue;
-        const uint32_t vw = A.bits[w];
+    const int64_t w = t * 32 + lane;
+    if (t * 32 < A.nw) {
+        // lane per word: fold its depth-plane words into binary digit words
+        // (bit b of D_k = bit k of the depth of vertex b relative to d0)
+        const uint32_t vw = w < A.nw ? __ldcs(A.bits + w) : 0u;
         uint32_t R = 0, D[5] = {0, 0, 0, 0, 0};
-        for (int64_t g0 = d0; g0 < nL; g0 += 8) {
-            uint32_t p[8];
+        for (int64_t g0 = d0; g0 < nL; g0 += kLvBatch) {
+            uint32_t p[kLvBatch];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) p[j] = g0 + j < nL ? depth_plane(A, g0 + j)[w] : 0u;
+            for (int j = 0; j < kLvBatch; ++j)
+                p[j] = w < A.nw && g0 + j < nL ? __ldcs(depth_plane(A, g0 + j).p + w) : 0u;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kLvBatch; ++j) {
                 const uint32_t rel = (uint32_t)(g0 + j - d0);
                 R |= p[j];
 #pragma unroll
                 for (int k = 0; k < 5; ++k) D[k] |= ((rel >> k) & 1u) ? p[j] : 0u;
             }
         }
-        int32_t lv[32];
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            uint32_t rel = 0;
-#pragma unroll
-            for (int k = 0; k < 5; ++k) rel |= ((D[k] >> b) & 1u) << k;
-            // reached: depth from the planes; visited otherwise: flushed earlier
-            lv[b] = ((R >> b) & 1u) ? (int32_t)(d0 + rel) : (((vw >> b) & 1u) ? -2 : -1);
-        }
-        int32_t *dst = A.level + w * 32;
+        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n &&  // warp-uniform
+                          (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
         if (fast) {
+            // round r: the warp writes words 8r..8r+7 of the tile; lane l takes
+            // levels 4(l%4)..+3 and 16+4(l%4)..+3 of word 8r + l/4, so each
+            // store instruction covers 8 full 64-byte half-rows
+            const int q = lane & 3;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                if ((lane >> 3) == r) {
-                    int32_t *row = st + (lane & 7) * kLvRow;
+                const int src = 8 * r + (lane >> 2);
+                const uint32_t Rs = __shfl_sync(0xffffffffu, R, src);
+                const uint32_t vs = __shfl_sync(0xffffffffu, vw, src);
+                uint32_t Ds[5];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<int4 *>(row)[q] =
-                            make_int4(lv[4 * q], lv[4 * q + 1], lv[4 * q + 2], lv[4 * q + 3]);
-                }
-                __syncwarp();
-                int32_t *gdst = A.level + (t * 32 + 8 * r) * 32;
+                for (int k = 0; k < 5; ++k) Ds[k] = __shfl_sync(0xffffffffu, D[k], src);
+                int4 *gdst = reinterpret_cast<int4 *>(A.level + (t * 32 + src) * 32);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int m = h * 4 + (lane >> 3);
-                    const int4 x = *reinterpret_cast<const int4 *>(st + m * kLvRow + (lane & 7) * 4);
-                    reinterpret_cast<int4 *>(gdst + m * 32)[lane & 7] = x;
+                    const int b0 = 16 * h + 4 * q;
+                    __stcs(gdst + 4 * h + q,
+                           make_int4(level_of(Rs, Ds, vs, d0, b0), level_of(Rs, Ds, vs, d0, b0 + 1),
+                                     level_of(Rs, Ds, vs, d0, b0 + 2), level_of(Rs, Ds, vs, d0, b0 + 3)));
                 }
-                __syncwarp();
             }
-        } else {
-            for (int b = 0; b < 32; ++b)
-                if (w * 32 + b < A.n && lv[b] != -2) dst[b] = lv[b];
+        } else if (w < A.nw) {
+            int32_t *dst = A.level + w * 32;
+            for (int b = 0; b < 32; ++b) {
+                const int32_t lv = level_of(R, D, vw, d0, b);
+                if (w * 32 + b < A.n && lv != -2) dst[b] = lv;
+            }
+        }
+    }
+    // last CTA out stamps the end of the pass (diagnostics)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&A.ctl->lv_done, 1u) == gridDim.x - 1) {
+            kstamp[4] = globaltimer();
+            A.ctl->lv_done = 0;
         }
     }
 }
@@ -1194,9 +1213,8 @@ __device__ void phase_levels(const Args<OffT> &A, int64_t nL, int32_t *stage) {
 template <typename OffT, int K, int MINB, bool SCAN>
 __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ TdSmem<OffT> sm;  // also the level pass's staging rows
-    static_assert(sizeof(TdSmem<OffT>) >= (kBlock / 32) * kLvStage * sizeof(int32_t),
-                  "level staging must fit the TD scratch");
+    extern __shared__ __align__(16) unsigned char dsm[];
+    TdSmem<OffT> &sm = *reinterpret_cast<TdSmem<OffT> *>(dsm);
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];  // per warp: found bits of its 32-word tile
     __shared__ int64_t s_pre[kCbMaxRanges + 1];
@@ -1331,13 +1349,6 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         ++rows;
     }
     if (leader) kstamp[2] = globaltimer();
-    if (S.v_f == 0 && !A.direct_levels) {  // finished in this launch: stamp the levels
-        grid.sync();
-        if (leader) kstamp[3] = globaltimer();
-        phase_levels(A, S.layer, reinterpret_cast<int32_t *>(&sm));
-        grid.sync();
-        if (leader) kstamp[4] = globaltimer();
-    }
     if (leader) {
         Ctl *c = A.ctl;
         c->layer = S.layer;
@@ -1402,6 +1413,7 @@ struct Workspace {
     int cb_ranges = 0;
     int64_t ncs = 0;  // chunk-start entries per queue buffer
     int grid = 0;
+    size_t smem = 0;
     const void *fn = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     void *h_ctl = nullptr;  // pinned mirror of ctl + rows
@@ -1411,6 +1423,12 @@ struct Workspace {
         if (h_ctl) cudaFreeHost(h_ctl);
     }
 };
+
+template <typename OffT>
+static size_t dyn_smem_bytes() {
+    size_t b = sizeof(TdSmem<OffT>);
+    return (b + 15) & ~(size_t)15;
+}
 
 static size_t ctl_bytes() { return sizeof(Ctl) + kRowsCap * sizeof(hbfs_layer_row); }
 
@@ -1455,7 +1473,11 @@ static int ws_alloc(hbfs_graph *g) {
         int vi = variant_index(n);
         if (vi < 0 || vi >= nv) vi = kDefaultVariant;
         w->fn = vt[vi].fn;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w->fn, kBlock, 0);
+        w->smem = dyn_smem_bytes<OffT>();
+        cudaError_t e = cudaFuncSetAttribute(w->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)w->smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w->fn, kBlock, w->smem);
         if (e != cudaSuccess || per_sm < 1)
             rc = set_error(HBFS_ECUDA, "occupancy query failed: %s", cudaGetErrorString(e));
         w->grid = per_sm * sms;
@@ -1532,7 +1554,13 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         A.do_init = launch == 0;
         void *kargs[] = {&A};
         HB_CUDA(cudaLaunchCooperativeKernel(w->fn, dim3(w->grid),
-                                            dim3(kBlock), kargs, 0, st));
+                                            dim3(kBlock), kargs, w->smem, st));
+        if (!A.direct_levels) {  // no-op unless this launch finished the traversal
+            const int64_t tiles = (g->nw + 31) / 32;
+            const int64_t per = kLvBlock / 32;
+            levels_kernel<OffT><<<(unsigned)((tiles + per - 1) / per), kLvBlock, 0, st>>>(A);
+            HB_CUDA(cudaGetLastError());
+        }
         HB_CUDA(cudaEventRecord(w->ev1, st));
         // Ctl plus the first rows in one copy; the rest only if needed.
         const size_t head = sizeof(Ctl) + 64 * sizeof(hbfs_layer_row);
