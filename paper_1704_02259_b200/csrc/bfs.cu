@@ -234,8 +234,14 @@ __device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
 
 // Bitmap probe through a raw pointer with a 32-bit word index: one wide
 // multiply-add per address instead of a 64-bit add chain.
+__device__ __forceinline__ uint32_t ld_global(const uint32_t *gp) {
+    uint32_t r;
+    asm("ld.global.u32 %0, [%1];" : "=r"(r) : "l"(gp));
+    return r;
+}
+// bm: a global-space address (pin_ptr), so the probe is an explicit LDG
 __device__ __forceinline__ uint32_t probe_word(const uint32_t *__restrict__ bm, uint32_t a) {
-    return bm[a >> 5];
+    return ld_global(bm + (a >> 5));
 }
 
 // Position of the (r+1)-th set bit of m (r < popc(m)); cheaper than __fns.
@@ -340,12 +346,12 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
     return x;
 }
 
-// Opaque copy of a pointer: the compiler cannot rematerialise it (it would
+// Opaque global-space copy of a pointer: the compiler cannot rematerialise it (it would
 // otherwise rebuild the bitmap plane address from the parameter bank with a
 // 64-bit add chain at every probe — 5 extra instructions per probe).
 __device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
     const uint32_t *q;
-    asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+    asm("cvta.to.global.u64 %0, %1;" : "=l"(q) : "l"(p));
     return q;
 }
 
@@ -1166,26 +1172,22 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
         const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n &&  // warp-uniform
                           (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
         if (fast) {
-            // round r: the warp writes words 8r..8r+7 of the tile; lane l takes
-            // levels 4(l%4)..+3 and 16+4(l%4)..+3 of word 8r + l/4, so each
-            // store instruction covers 8 full 64-byte half-rows
-            const int q = lane & 3;
+            // round r: the warp writes words 4r..4r+3 of the tile (512
+            // contiguous bytes, four full lines); lane l takes levels
+            // 4(l%8)..+3 of word 4r + l/8
+            const int q = lane & 7;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int src = 8 * r + (lane >> 2);
+            for (int r = 0; r < 8; ++r) {
+                const int src = 4 * r + (lane >> 3);
                 const uint32_t Rs = __shfl_sync(0xffffffffu, R, src);
                 const uint32_t vs = __shfl_sync(0xffffffffu, vw, src);
                 uint32_t Ds[5];
 #pragma unroll
                 for (int k = 0; k < 5; ++k) Ds[k] = __shfl_sync(0xffffffffu, D[k], src);
                 int4 *gdst = reinterpret_cast<int4 *>(A.level + (t * 32 + src) * 32);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int b0 = 16 * h + 4 * q;
-                    __stcs(gdst + 4 * h + q,
-                           make_int4(level_of(Rs, Ds, vs, d0, b0), level_of(Rs, Ds, vs, d0, b0 + 1),
-                                     level_of(Rs, Ds, vs, d0, b0 + 2), level_of(Rs, Ds, vs, d0, b0 + 3)));
-                }
+                const int b0 = 4 * q;
+                __stcs(gdst + q, make_int4(level_of(Rs, Ds, vs, d0, b0), level_of(Rs, Ds, vs, d0, b0 + 1),
+                                           level_of(Rs, Ds, vs, d0, b0 + 2), level_of(Rs, Ds, vs, d0, b0 + 3)));
             }
         } else if (w < A.nw) {
             int32_t *dst = A.level + w * 32;
