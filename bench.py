@@ -435,7 +435,7 @@ def run_distributed(args, cfg):
             "data": "synthetic (bit-exact reference R-MAT generator on device, seed 1)",
             "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
                        "roots": ROOTS, "heuristic": cfg["heur"], "parent_mode": "minid",
-                       "parallelism": f"1d-partition x{ws} (NCCL all-gather / reduce-scatter MIN / all-reduce)",
+                       "parallelism": f"1d-partition x{ws} (NCCL all-gather / all-to-all-v records / all-reduce)",
                        "l2": "flushed (256 MB write) before every traversal"},
             "gpu_launches": None,
             "wall_s_timed_region": wall,

@@ -149,10 +149,11 @@ int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows);
 /* ---- multi-GPU: one rank's share of a 1D vertex partition ----
  * Rank r owns vertices [lo, hi) (word aligned) with their CSR rows (global
  * column ids); frontier and visited bitmaps are replicated, parent/level owned.
- * The host runs, per layer, hbfs_part_bu or hbfs_part_td_expand + (NCCL
- * reduce-scatter MIN of the candidates) + hbfs_part_td_finish, then (NCCL
- * all-gather of the next-frontier slices) + hbfs_part_absorb and an all-reduce
- * of the counters — paper_1704_02259_b200/mgpu.py.  Replaces, for P > 1, the
+ * The host runs, per layer, hbfs_part_bu, or hbfs_part_td_expand + (all-to-all
+ * of the per-owner counts) + hbfs_part_td_pack + (NCCL all-to-all-v of the
+ * 8-byte records) + hbfs_part_td_apply; then (NCCL all-gather of the
+ * next-frontier slices) + hbfs_part_absorb and an all-reduce of the counters
+ * — paper_1704_02259_b200/mgpu.py.  Replaces, for P > 1, the
  * same reference interfaces as hbfs_graph_build / hbfs_bfs. */
 typedef struct hbfs_part hbfs_part;
 
@@ -174,12 +175,17 @@ int hbfs_part_init(hbfs_part *p, int64_t root, void *stream);
  * degree sum, gathers, fallbacks} (the reference's 16-lane counters). */
 int hbfs_part_bu(hbfs_part *p, int32_t depth, int32_t max_pos, uint32_t *next_slice,
                  unsigned long long *counters, void *stream);
-/* Top-down expansion of the owned frontier: cand (device int32[n], pre-filled
- * with INT32_MAX) receives atomicMin(parent id) for every unvisited target. */
-int hbfs_part_td_expand(hbfs_part *p, int32_t *cand, void *stream);
-/* Apply this rank's MIN-reduced candidate slice (device int32[hi-lo]). */
-int hbfs_part_td_finish(hbfs_part *p, int32_t depth, const int32_t *cand_slice,
-                        uint32_t *next_slice, unsigned long long *counters, void *stream);
+/* Top-down expansion of the owned frontier for a `world`-rank partition:
+ * every unvisited target is queued once for its owner with this rank's min
+ * parent candidate; send_counts: device int64[world] = records per owner. */
+int hbfs_part_td_expand(hbfs_part *p, int32_t world, int64_t *send_counts, void *stream);
+/* records: device uint64[sum(send_counts)] = parent << 32 | vertex, packed by
+ * owner rank (the all-to-all-v send buffer). */
+int hbfs_part_td_pack(hbfs_part *p, uint64_t *records, void *stream);
+/* Apply the nrec records received from all ranks (owned vertices): min-id
+ * parents, levels, next slice; counters: device uint64[4]. */
+int hbfs_part_td_apply(hbfs_part *p, int32_t depth, const uint64_t *records, int64_t nrec,
+                       uint32_t *next_slice, unsigned long long *counters, void *stream);
 /* next_full: device uint32[ceil(n/32)] all-gathered next frontier. */
 int hbfs_part_absorb(hbfs_part *p, const uint32_t *next_full, void *stream);
 /* Owned parent/level (hi-lo entries each). */

@@ -1,7 +1,8 @@
 """TEST INFRASTRUCTURE — CPU rank for the multi-GPU controller (mgpu.DistBfs).
 
 Implements the same per-rank steps as csrc/part.cu (bottom-up over owned words,
-top-down min-candidate expansion, candidate finish, frontier absorb) in numpy
+top-down expansion into per-owner (parent, vertex) records, record apply,
+frontier absorb) in numpy
 on a slice of a host CSR, so the partitioned host logic (exchange order,
 padding, counters, decisions) runs under gloo with world_size > 1 on CPU.  The
 semantics restated are the reference's layer kernels (_native.pyx:65-204) on an
@@ -87,28 +88,49 @@ class CpuRankOps:
         next_slice.copy_(self._torch().from_numpy(nxt.view(np.int32)))
         ctr.copy_(self._torch().tensor([found, degsum, gathers, fallbacks], dtype=self._torch().int64))
 
-    def td_expand(self, cand):
-        c = cand.numpy()
+    def td_expand(self, world, send_counts):
+        """Unvisited targets of the owned frontier, each once per owner with
+        this rank's min parent candidate (csrc/part.cu kp_td)."""
+        from paper_1704_02259_b200.mgpu import partition
+
+        best = {}
         owned = _bits_to_ids(self.F, self.n)
         owned = owned[(owned >= self.lo) & (owned < self.hi)]
         for u in owned:
             lv = u - self.lo
             row = self.adj[self.rs[lv]:self.rs[lv + 1]]
             row = row[~self._test(self.V, row)]
-            if len(row):
-                np.minimum.at(c, row.astype(np.int64), np.int32(u))
+            for v in row.tolist():
+                if v not in best or u < best[v]:
+                    best[v] = int(u)
+        span = partition(self.n, world, 0)[2] * 32
+        self._send = [[] for _ in range(world)]
+        for v in sorted(best):
+            self._send[v // span].append((best[v] << 32) | v)
+        send_counts.copy_(self._torch().tensor([len(q) for q in self._send], dtype=self._torch().int64))
 
-    def td_finish(self, depth, cand_slice, next_slice, ctr):
-        cs = cand_slice.numpy()[: self.nloc]
+    def td_pack(self, records):
+        flat = [r for q in self._send for r in q]
+        if flat:
+            records[: len(flat)].copy_(self._torch().tensor(flat, dtype=self._torch().int64))
+
+    def td_apply(self, depth, records, nrec, next_slice, ctr):
+        rec = records.numpy()[:nrec].astype(np.uint64)
         nxt = np.zeros(len(next_slice), dtype=np.uint32)
-        hit = np.flatnonzero(cs != INT32_MAX)
-        self.parent[hit] = cs[hit].astype(np.uint32)
-        self.level[hit] = depth + 1
-        for lv in hit:
+        best = {}
+        for r in rec.tolist():
+            v, u = r & 0xFFFFFFFF, r >> 32
+            if v not in best or u < best[v]:
+                best[v] = u
+        deg = 0
+        for v, u in best.items():
+            lv = v - self.lo
+            self.parent[lv] = u
+            self.level[lv] = depth + 1
             nxt[lv >> 5] |= np.uint32(1 << (lv & 31))
-        deg = (self.rs[hit + 1] - self.rs[hit]).sum() if len(hit) else 0
+            deg += int(self.rs[lv + 1] - self.rs[lv])
         next_slice.copy_(self._torch().from_numpy(nxt.view(np.int32)))
-        ctr.copy_(self._torch().tensor([len(hit), int(deg), 0, 0], dtype=self._torch().int64))
+        ctr.copy_(self._torch().tensor([len(best), deg, 0, 0], dtype=self._torch().int64))
 
     def absorb(self, next_full):
         f = next_full.numpy().view(np.uint32)[: self.W].copy()

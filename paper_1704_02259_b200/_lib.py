@@ -77,8 +77,9 @@ SIGNATURES = {
     "hbfs_part_free": (C.c_int, [P]),
     "hbfs_part_init": (C.c_int, [P, i64, P]),
     "hbfs_part_bu": (C.c_int, [P, i32, i32, P, P, P]),
-    "hbfs_part_td_expand": (C.c_int, [P, P, P]),
-    "hbfs_part_td_finish": (C.c_int, [P, i32, P, P, P, P]),
+    "hbfs_part_td_expand": (C.c_int, [P, i32, P, P]),
+    "hbfs_part_td_pack": (C.c_int, [P, P, P]),
+    "hbfs_part_td_apply": (C.c_int, [P, i32, P, i64, P, P, P]),
     "hbfs_part_absorb": (C.c_int, [P, P, P]),
     "hbfs_part_outputs": (C.c_int, [P, P, P, C.c_int, P]),
 }

@@ -4,15 +4,21 @@
 // global column ids.  The frontier bitmap F and the visited bitmap V are
 // replicated (n bits each); parent/level are owned-only.  Per layer the host
 // (paper_1704_02259_b200/mgpu.py) runs one of
-//   bottom-up:  hbfs_part_bu         -> next-frontier slice of the owned words
-//   top-down:   hbfs_part_td_expand  -> n-sized min-candidate array (int32,
-//                                       INT32_MAX = none) for unvisited targets
-//               [NCCL reduce-scatter(MIN) of the candidates to their owners]
-//               hbfs_part_td_finish  -> owned parents/levels + next slice
+//   bottom-up:  hbfs_part_bu        -> next-frontier slice of the owned words
+//   top-down:   hbfs_part_td_expand -> per-owner queues of the unvisited
+//                                      targets, each once, with its min parent
+//                                      candidate; counts per owner
+//               [all-to-all of the counts]
+//               hbfs_part_td_pack   -> 8-byte (parent, vertex) records packed
+//                                      by owner
+//               [NCCL all-to-all-v of the records]
+//               hbfs_part_td_apply  -> owned parents/levels + next slice
 // then [NCCL all-gather of the slices] and hbfs_part_absorb (F = next,
-// V |= next), plus an all-reduce of the four layer counters.  Parents are the
-// global min-id neighbour one level up: bottom-up takes the first
-// frontier hit in the sorted row, top-down the MIN over all ranks' arcs.
+// V |= next), plus an all-reduce of the four layer counters.  Top-down traffic
+// is 8 bytes per (rank, newly reached vertex) pair, not O(n) per layer.
+// Parents are the global min-id neighbour one level up: bottom-up
+// takes the first frontier hit in the sorted row, top-down the MIN over every
+// rank's arcs (each rank pre-reduces its own, the owner reduces the records).
 // Replaces, for P > 1, the same reference functions as bfs.cu.
 #include <cub/cub.cuh>
 
@@ -30,6 +36,14 @@ struct Part {
     DevBuf parent, level;     // owned
     DevBuf q;                 // uint32[nloc] owned frontier queue
     DevBuf scratch;           // counters etc.
+    // top-down exchange state (all kept clean between layers)
+    DevBuf cand;              // int32[n]  min parent candidate per target (INT32_MAX = none)
+    DevBuf touch;             // uint32[W] target already queued this layer
+    DevBuf candown;           // int32[nloc] min over the received records
+    DevBuf sendq;             // uint32[world * span] per-owner target queues
+    DevBuf scnt;              // uint64[world] per-owner queue fill
+    int world = 0;            // partition the queues were sized for
+    int64_t span = 0;         // vertices per owner block (word aligned)
 };
 
 static inline int pgrid(int64_t items, int block = 256) {
@@ -203,9 +217,25 @@ __global__ void kp_queue(int64_t wloc, int64_t lo, const uint32_t *F, uint32_t *
 }
 
 // Top-down expansion: warp per frontier row for short rows, the whole CTA for
-// rows of >= 1024 arcs; every arc into an unvisited target lowers cand[v].
+// rows of >= 1024 arcs.  Every arc into an unvisited target lowers cand[v];
+// the first arc to reach v this layer (touch bit) appends v to its owner's
+// queue, so each target is sent once per rank with its rank-local min parent.
+__device__ __forceinline__ void td_arc(uint32_t v, int32_t u, const uint32_t *V, int32_t *cand,
+                                       uint32_t *touch, uint32_t *sendq, unsigned long long *scnt,
+                                       int64_t span) {
+    const uint32_t b = 1u << (v & 31);
+    if ((V[v >> 5] & b)) return;
+    atomicMin(&cand[v], u);
+    if (__ldcg(&touch[v >> 5]) & b) return;
+    if (atomicOr(&touch[v >> 5], b) & b) return;
+    const int64_t o = (int64_t)v / span;
+    const unsigned long long i = atomicAdd(&scnt[o], 1ull);
+    sendq[o * span + (int64_t)i] = v;
+}
+
 __global__ void kp_td(const uint32_t *q, int64_t qn, int64_t lo, const uint64_t *rs,
-                      const uint32_t *adj, const uint32_t *V, int32_t *cand, int big) {
+                      const uint32_t *adj, const uint32_t *V, int32_t *cand, uint32_t *touch,
+                      uint32_t *sendq, unsigned long long *scnt, int64_t span, int big) {
     const int lane = threadIdx.x & 31;
     if (!big) {
         for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
@@ -214,10 +244,7 @@ __global__ void kp_td(const uint32_t *q, int64_t qn, int64_t lo, const uint64_t 
             const uint64_t s = rs[ul], e = rs[ul + 1];
             if (e - s >= 1024) continue;
             const int32_t u = (int32_t)(lo + ul);
-            for (uint64_t k = s + lane; k < e; k += 32) {
-                const uint32_t v = adj[k];
-                if (!((V[v >> 5] >> (v & 31)) & 1u)) atomicMin(&cand[v], u);
-            }
+            for (uint64_t k = s + lane; k < e; k += 32) td_arc(adj[k], u, V, cand, touch, sendq, scnt, span);
         }
     } else {
         for (int64_t i = blockIdx.x; i < qn; i += gridDim.x) {
@@ -225,43 +252,68 @@ __global__ void kp_td(const uint32_t *q, int64_t qn, int64_t lo, const uint64_t 
             const uint64_t s = rs[ul], e = rs[ul + 1];
             if (e - s < 1024) continue;
             const int32_t u = (int32_t)(lo + ul);
-            for (uint64_t k = s + threadIdx.x; k < e; k += blockDim.x) {
-                const uint32_t v = adj[k];
-                if (!((V[v >> 5] >> (v & 31)) & 1u)) atomicMin(&cand[v], u);
-            }
+            for (uint64_t k = s + threadIdx.x; k < e; k += blockDim.x)
+                td_arc(adj[k], u, V, cand, touch, sendq, scnt, span);
         }
     }
 }
 
-// Owned slice of the MIN-reduced candidates -> parents, levels, next slice.
-__global__ void kp_td_finish(int64_t wloc, int64_t nloc, int32_t depth1, const int32_t *cand,
-                             const uint64_t *rs,
-                             uint32_t *parent, int32_t *level, uint32_t *next,
-                             unsigned long long *ctr) {
-    const int lane = threadIdx.x & 31;
+// Records of the queued targets, packed by owner (record = parent << 32 | v);
+// resets cand and touch behind itself.
+__global__ void kp_td_pack(int world, int64_t span, const uint32_t *sendq,
+                           const unsigned long long *scnt, int32_t *cand, uint32_t *touch,
+                           unsigned long long *rec) {
+    int64_t total = 0;
+    for (int o = 0; o < world; ++o) total += (int64_t)scnt[o];
+    PSTRIDE(k, total) {
+        int64_t base = 0;
+        int o = 0;
+        while (k - base >= (int64_t)scnt[o]) base += (int64_t)scnt[o++];
+        const uint32_t v = sendq[o * span + (k - base)];
+        rec[k] = ((unsigned long long)(uint32_t)cand[v] << 32) | v;
+        cand[v] = 0x7FFFFFFF;
+        touch[v >> 5] = 0u;
+    }
+}
+
+// Owner side, pass 1: MIN over every rank's record for the same vertex.
+__global__ void kp_td_recv_min(const unsigned long long *rec, int64_t nrec, int64_t lo,
+                               int32_t *candown) {
+    PSTRIDE(k, nrec) {
+        const unsigned long long r = rec[k];
+        atomicMin(&candown[(int64_t)(uint32_t)r - lo], (int32_t)(r >> 32));
+    }
+}
+
+// Owner side, pass 2: the first record of each vertex claims it (next-slice
+// bit), writes parent/level from the reduced candidate and resets it.
+__global__ void kp_td_recv_claim(const unsigned long long *rec, int64_t nrec, int64_t lo,
+                                 int32_t depth1, const uint64_t *rs, int32_t *candown,
+                                 uint32_t *parent, int32_t *level, uint32_t *next,
+                                 unsigned long long *ctr) {
     unsigned long long c_cnt = 0, c_deg = 0;
-    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < wloc;
-         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t lv = j * 32 + lane;
-        const int32_t c = lv < nloc ? cand[lv] : 0x7FFFFFFF;
-        const bool found = c != 0x7FFFFFFF;
-        if (found) {
-            parent[lv] = (uint32_t)c;
-            level[lv] = depth1;
-            c_cnt += 1;
-            c_deg += (unsigned long long)(rs[lv + 1] - rs[lv]);
-        }
-        const unsigned fm = __ballot_sync(0xffffffffu, found);
-        if (lane == 0) next[j] = fm;
+    PSTRIDE(k, nrec) {
+        const int64_t lv = (int64_t)(uint32_t)rec[k] - lo;
+        const uint32_t b = 1u << (lv & 31);
+        if (atomicOr(&next[lv >> 5], b) & b) continue;
+        parent[lv] = (uint32_t)candown[lv];
+        level[lv] = depth1;
+        candown[lv] = 0x7FFFFFFF;
+        c_cnt += 1;
+        c_deg += (unsigned long long)(rs[lv + 1] - rs[lv]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         c_cnt += __shfl_down_sync(0xffffffffu, c_cnt, o);
         c_deg += __shfl_down_sync(0xffffffffu, c_deg, o);
     }
-    if (lane == 0) {
+    if ((threadIdx.x & 31) == 0) {
         if (c_cnt) atomicAdd(&ctr[0], c_cnt);
         if (c_deg) atomicAdd(&ctr[1], c_deg);
     }
+}
+
+__global__ void kp_fill_i32(int32_t *p, int64_t n, int32_t x) {
+    PSTRIDE(i, n) p[i] = x;
 }
 
 __global__ void kp_absorb(int64_t W, const uint32_t *next, uint32_t *F, uint32_t *V) {
@@ -279,6 +331,13 @@ static int part_alloc_state(Part *P) {
     HB_CHECK(P->level.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->q.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->scratch.alloc(64));
+    HB_CHECK(P->cand.alloc(P->n * 4 + 16));
+    HB_CHECK(P->touch.alloc(P->W * 4 + 16));
+    HB_CHECK(P->candown.alloc(P->nloc * 4 + 16));
+    kp_fill_i32<<<pgrid(P->n), 256>>>(P->cand.as<int32_t>(), P->n, 0x7FFFFFFF);
+    kp_fill_i32<<<pgrid(P->nloc), 256>>>(P->candown.as<int32_t>(), P->nloc, 0x7FFFFFFF);
+    HB_CUDA(cudaMemset(P->touch.p, 0, P->W * 4));
+    HB_CUDA(cudaDeviceSynchronize());
     return HBFS_OK;
 }
 
@@ -494,13 +553,25 @@ extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32
     HB_ENTRY_END
 }
 
-// cand: device int32[n], pre-filled with INT32_MAX by the caller
-extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t *cand, void *stream) {
+// Top-down expansion of the owned frontier for a `world`-rank partition (owner
+// blocks of `span` = partition() words * 32 vertices).  send_counts: device
+// int64[world], records queued per owner.
+extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t world, int64_t *send_counts, void *stream) {
     HB_ENTRY_BEGIN
-    if (!P || !cand) return set_error(HBFS_EINVAL, "bad arguments");
+    if (!P || !send_counts || world < 1) return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t wper = (P->W + world - 1) / world;
+    const int64_t span = wper * 32;
+    if (P->world != world) {
+        HB_CHECK(P->sendq.alloc(world * span * 4 + 16));
+        HB_CHECK(P->scnt.alloc(world * 8 + 16));
+        P->world = world;
+        P->span = span;
+    }
+    unsigned long long *scnt = P->scnt.as<unsigned long long>();
     unsigned long long *qn = P->scratch.as<unsigned long long>();
     HB_CUDA(cudaMemsetAsync(qn, 0, 8, st));
+    HB_CUDA(cudaMemsetAsync(scnt, 0, world * 8, st));
     kp_queue<<<pgrid(P->wloc), 256, 0, st>>>(P->wloc, P->lo, P->F.as<uint32_t>(),
                                              P->q.as<uint32_t>(), qn);
     HB_CUDA(cudaGetLastError());
@@ -510,28 +581,52 @@ extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t *cand, void *stream) {
     if (h > 0) {
         kp_td<<<pgrid((int64_t)h * 32), 256, 0, st>>>(P->q.as<uint32_t>(), (int64_t)h, P->lo,
                                                       P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-                                                      P->V.as<uint32_t>(), cand, 0);
+                                                      P->V.as<uint32_t>(), P->cand.as<int32_t>(),
+                                                      P->touch.as<uint32_t>(), P->sendq.as<uint32_t>(),
+                                                      scnt, span, 0);
         kp_td<<<(int)std::min<int64_t>((int64_t)h, 148 * 8), 512, 0, st>>>(
             P->q.as<uint32_t>(), (int64_t)h, P->lo, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-            P->V.as<uint32_t>(), cand, 1);
+            P->V.as<uint32_t>(), P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
+            P->sendq.as<uint32_t>(), scnt, span, 1);
         HB_CUDA(cudaGetLastError());
     }
+    HB_CUDA(cudaMemcpyAsync(send_counts, scnt, world * 8, cudaMemcpyDeviceToDevice, st));
     return HBFS_OK;
     HB_ENTRY_END
 }
 
-// cand_slice: device int32[nloc] (this rank's MIN-reduced candidates)
-extern "C" int hbfs_part_td_finish(hbfs_part *P, int32_t depth, const int32_t *cand_slice,
-                                   uint32_t *next_slice, unsigned long long *counters,
-                                   void *stream) {
+// records: device uint64[sum(send_counts)], packed by owner; resets the
+// expansion state for the next layer.
+extern "C" int hbfs_part_td_pack(hbfs_part *P, uint64_t *records, void *stream) {
     HB_ENTRY_BEGIN
-    if (!P || !cand_slice || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
+    if (!P || !records || P->world < 1) return set_error(HBFS_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    kp_td_pack<<<pgrid(P->nloc), 256, 0, st>>>(P->world, P->span, P->sendq.as<uint32_t>(),
+                                               P->scnt.as<unsigned long long>(),
+                                               P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
+                                               reinterpret_cast<unsigned long long *>(records));
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// records: device uint64[nrec] received from every rank (vertices owned here).
+extern "C" int hbfs_part_td_apply(hbfs_part *P, int32_t depth, const uint64_t *records,
+                                  int64_t nrec, uint32_t *next_slice,
+                                  unsigned long long *counters, void *stream) {
+    HB_ENTRY_BEGIN
+    if (!P || (!records && nrec) || nrec < 0 || !next_slice || !counters)
+        return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     HB_CUDA(cudaMemsetAsync(counters, 0, 32, st));
-    kp_td_finish<<<pgrid(P->wloc * 32), 256, 0, st>>>(P->wloc, P->nloc, depth + 1, cand_slice,
-                                                      P->rs.as<uint64_t>(), P->parent.as<uint32_t>(),
+    if (nrec > 0) {
+        const unsigned long long *r = reinterpret_cast<const unsigned long long *>(records);
+        kp_td_recv_min<<<pgrid(nrec), 256, 0, st>>>(r, nrec, P->lo, P->candown.as<int32_t>());
+        kp_td_recv_claim<<<pgrid(nrec), 256, 0, st>>>(r, nrec, P->lo, depth + 1, P->rs.as<uint64_t>(),
+                                                      P->candown.as<int32_t>(), P->parent.as<uint32_t>(),
                                                       P->level.as<int32_t>(), next_slice, counters);
-    HB_CUDA(cudaGetLastError());
+        HB_CUDA(cudaGetLastError());
+    }
     return HBFS_OK;
     HB_ENTRY_END
 }

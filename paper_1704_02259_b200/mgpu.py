@@ -7,8 +7,11 @@ hybrid.py:83-175, with the same trace):
 
 * bottom-up: local bottom-up over the owned words against the replicated
   frontier (parents need no communication: rows are local, SURVEY F1);
-* top-down: local expansion of the owned frontier into an n-sized min-candidate
-  array, **reduce-scatter(MIN)** to the owners (exact min-id parents);
+* top-down: local expansion of the owned frontier; every unvisited target is
+  queued once for its owner with this rank's min parent candidate, the counts
+  go **all-to-all** and the 8-byte (parent, vertex) records **all-to-all-v**;
+  the owner takes the MIN per vertex (exact min-id parents).  Traffic is
+  proportional to the newly reached vertices, never O(n) per layer;
 * then **all-gather** of the next-frontier slices (the new replicated frontier,
   also OR-ed into the replicated visited bitmap) and an **all-reduce(SUM)** of
   the four layer counters, so every rank takes the same direction decision.
@@ -33,7 +36,6 @@ import numpy as np
 from .hybrid import BOTTOM_UP, TOP_DOWN, HEURISTICS, COUNTER_MODES, HeuristicParams, LayerTraceRow
 from .lanes import VecConfig
 
-INT32_MAX = 0x7FFFFFFF
 
 
 def partition(n: int, world: int, rank: int):
@@ -94,18 +96,23 @@ class TorchComm:
             self.dist.all_gather(list(out.chunk(self.world)), s, group=self.group)
         return [out]
 
-    def reduce_scatter_min(self, fulls):
-        full = fulls[0]
-        chunk = full.numel() // self.world
-        if self.backend == "nccl":
-            import torch
+    def all_to_all_counts(self, counts):
+        """counts[0]: int64[world] sent by this rank to each rank -> int64[world]
+        received from each rank."""
+        import torch
 
-            out = torch.empty(chunk, dtype=full.dtype, device=full.device)
-            self.dist.reduce_scatter_tensor(out, full, op=self.dist.ReduceOp.MIN, group=self.group)
-            return [out]
-        # gloo has no reduce_scatter: all-reduce then keep the owned chunk
-        self.dist.all_reduce(full, op=self.dist.ReduceOp.MIN, group=self.group)
-        return [full[self.rank * chunk:(self.rank + 1) * chunk].clone()]
+        out = torch.empty_like(counts[0])
+        self.dist.all_to_all_single(out, counts[0], group=self.group)
+        return [out]
+
+    def all_to_all_v(self, sendbufs, send_splits, recv_splits):
+        import torch
+
+        s = sendbufs[0]
+        out = torch.empty(max(1, sum(recv_splits[0])), dtype=s.dtype, device=s.device)
+        self.dist.all_to_all_single(out[: sum(recv_splits[0])], s[: sum(send_splits[0])],
+                                    recv_splits[0], send_splits[0], group=self.group)
+        return [out]
 
     def all_reduce_sum(self, tensors):
         self.dist.all_reduce(tensors[0], op=self.dist.ReduceOp.SUM, group=self.group)
@@ -136,13 +143,27 @@ class LocalComm:
         full = torch.cat(list(slices))
         return [full.clone() for _ in slices]
 
-    def reduce_scatter_min(self, fulls):
+    def all_to_all_counts(self, counts):
         import torch
 
-        m = fulls[0].clone()
-        for f in fulls[1:]:
-            m = torch.minimum(m, f)
-        return [c.clone() for c in m.chunk(self.world)]
+        m = torch.stack(list(counts))  # m[src, dst]
+        return [m[:, r].clone() for r in range(self.world)]
+
+    def all_to_all_v(self, sendbufs, send_splits, recv_splits):
+        import torch
+
+        segs = []  # segs[src][dst]
+        for b, sp in zip(sendbufs, send_splits):
+            offs = [0]
+            for x in sp:
+                offs.append(offs[-1] + x)
+            segs.append([b[offs[d]:offs[d + 1]] for d in range(self.world)])
+        outs = []
+        for d in range(self.world):
+            parts = [segs[src][d] for src in range(self.world)]
+            out = torch.cat(parts) if sum(p.numel() for p in parts) else sendbufs[d].new_empty(1)
+            outs.append(out)
+        return outs
 
     def all_reduce_sum(self, tensors):
         tot = tensors[0].clone()
@@ -245,13 +266,17 @@ class CudaRankOps:
         self._lib.check(self.lib.hbfs_part_bu(self.h, depth, max_pos, C.c_void_p(next_slice.data_ptr()),
                                               C.c_void_p(ctr.data_ptr()), self._s()))
 
-    def td_expand(self, cand):
-        self._lib.check(self.lib.hbfs_part_td_expand(self.h, C.c_void_p(cand.data_ptr()), self._s()))
+    def td_expand(self, world, send_counts):
+        self._lib.check(self.lib.hbfs_part_td_expand(self.h, world, C.c_void_p(send_counts.data_ptr()),
+                                                     self._s()))
 
-    def td_finish(self, depth, cand_slice, next_slice, ctr):
-        self._lib.check(self.lib.hbfs_part_td_finish(self.h, depth, C.c_void_p(cand_slice.data_ptr()),
-                                                     C.c_void_p(next_slice.data_ptr()),
-                                                     C.c_void_p(ctr.data_ptr()), self._s()))
+    def td_pack(self, records):
+        self._lib.check(self.lib.hbfs_part_td_pack(self.h, C.c_void_p(records.data_ptr()), self._s()))
+
+    def td_apply(self, depth, records, nrec, next_slice, ctr):
+        self._lib.check(self.lib.hbfs_part_td_apply(self.h, depth, C.c_void_p(records.data_ptr()), nrec,
+                                                    C.c_void_p(next_slice.data_ptr()),
+                                                    C.c_void_p(ctr.data_ptr()), self._s()))
 
     def absorb(self, next_full):
         self._lib.check(self.lib.hbfs_part_absorb(self.h, C.c_void_p(next_full.data_ptr()), self._s()))
@@ -324,7 +349,7 @@ class DistBfs:
         v_f, e_f, eu_v, eu_e, prev_vf, cur = 1, rdeg, self.n - 1, self.arcs_global - rdeg, 0, 0
         slices = [r.new_tensor(self.wper, "int32") for r in R]
         ctrs = [r.new_tensor(4, "int64") for r in R]
-        cands = None
+        scounts = [r.new_tensor(self.world, "int64") for r in R]
         trace = []
         layer = 0
         while v_f > 0:
@@ -336,14 +361,19 @@ class DistBfs:
                 for r, s, c in zip(R, slices, ctrs):
                     r.bu(layer, cfg.max_pos, s, c)
             else:
-                if cands is None:
-                    cands = [r.new_tensor(self.world * self.wper * 32, "int32") for r in R]
-                for r, cd in zip(R, cands):
-                    cd.fill_(INT32_MAX)
-                    r.td_expand(cd)
-                owned = self.comm.reduce_scatter_min(cands)
-                for r, o, s, c in zip(R, owned, slices, ctrs):
-                    r.td_finish(layer, o, s, c)
+                for r, sc in zip(R, scounts):
+                    r.td_expand(self.world, sc)
+                rcounts = self.comm.all_to_all_counts(scounts)
+                send_splits = [sc.tolist() for sc in scounts]
+                recv_splits = [rc.tolist() for rc in rcounts]
+                sends = []
+                for r, sp in zip(R, send_splits):
+                    b = r.new_tensor(max(1, sum(sp)), "int64")
+                    r.td_pack(b)
+                    sends.append(b)
+                recvs = self.comm.all_to_all_v(sends, send_splits, recv_splits)
+                for r, rb, rp, s, c in zip(R, recvs, recv_splits, slices, ctrs):
+                    r.td_apply(layer, rb, sum(rp), s, c)
             fulls = self.comm.all_gather(slices)
             self.comm.all_reduce_sum(ctrs)
             for r, f in zip(R, fulls):

@@ -1,7 +1,8 @@
 """Multi-rank (1D partition) controller on CPU: world_size 2 and 4 over gloo.
 
 The host logic of paper_1704_02259_b200.mgpu (partitioning, the per-layer
-exchange: reduce-scatter(MIN) of top-down candidates, all-gather of the
+exchange: all-to-all of per-owner counts and all-to-all-v of the top-down
+(parent, vertex) records, all-gather of the
 next-frontier slices, all-reduce of the switch counters) runs with CPU ranks
 (oracle/part_cpu.py) and must reproduce the single-process reference
 traversal bit for bit: levels, min-id parents and the trace.
