@@ -146,6 +146,31 @@ int hbfs_traversal_bytes_layers(hbfs_graph *g, int64_t root, const int32_t *leve
  * 0 = phase not taken).  rows <= 1024. */
 int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows);
 
+/* ---- per-layer steps on caller buffers: the hybfs._native surface ----
+ * All pointers are DEVICE pointers in the reference's layout: rs int64[n+1],
+ * adj uint32[arcs], LSB-first bitmaps uint32[ceil(n/32)] (frontier.py:3-6),
+ * parent uint32[n].  vis/out/parent are updated in place exactly as the
+ * reference's single-threaded loops leave them.  Synchronous on `stream`. */
+
+/* _native.top_down_layer / top_down_chunked (_native.pyx:65-86, :207-239):
+ * every unvisited neighbour v of the frontier `in` joins vis and out with
+ * parent = its smallest frontier neighbour (the first claimer of the
+ * ascending loop).  gathers (may be NULL) = the chunked kernel's count = the
+ * frontier's degree sum. */
+int hbfs_layer_top_down(const int64_t *rs, const uint32_t *adj, const uint32_t *in, uint32_t *vis,
+                        uint32_t *out, uint32_t *parent, int64_t n, int64_t *gathers, void *stream);
+/* _native.bottom_up_layer / bottom_up_multiple_set (_native.pyx:89-204): every
+ * unvisited v whose sorted row holds a frontier vertex takes the first one as
+ * parent and joins vis and out.  fallback/gathers (may be NULL): the 16-lane
+ * kernel's counters for probe depth max_pos >= 1. */
+int hbfs_layer_bottom_up(const int64_t *rs, const uint32_t *adj, const uint32_t *in, uint32_t *vis,
+                         uint32_t *out, uint32_t *parent, int64_t n, int32_t max_pos,
+                         int64_t *fallback, int64_t *gathers, void *stream);
+/* _native.bfs_reference (_native.pyx:39-62): levels, and parents in the FIFO
+ * queue's first-discoverer order (parent/level: device uint32[n] / int32[n]). */
+int hbfs_reference_bfs(const int64_t *rs, const uint32_t *adj, int64_t n, int64_t source,
+                       uint32_t *parent, int32_t *level, void *stream);
+
 /* ---- multi-GPU: one rank's share of a 1D vertex partition ----
  * Rank r owns vertices [lo, hi) (word aligned) with their CSR rows (global
  * column ids); frontier and visited bitmaps are replicated, parent/level owned.

@@ -337,6 +337,28 @@ static void bu_multiple_set(const int64_t *rs, const uint32_t *adj, int64_t n, i
     }
 }
 
+/* Exported per-layer steps (test checkers for csrc/layer.cu). */
+int64_t hbo_td_layer(const int64_t *rs, const uint32_t *adj, int64_t n, const uint32_t *inw,
+                     uint32_t *vis, uint32_t *out, uint32_t *parent)
+{
+    return td_layer(rs, adj, (n + 31) / 32, inw, vis, out, parent);
+}
+
+void hbo_bu_layer(const int64_t *rs, const uint32_t *adj, int64_t n, const uint32_t *inw,
+                  uint32_t *vis, uint32_t *out, uint32_t *parent)
+{
+    bu_scalar(rs, adj, n, inw, vis, out, parent);
+}
+
+void hbo_bu_multiple_set(const int64_t *rs, const uint32_t *adj, int64_t n, int max_pos,
+                         const uint32_t *posw, const uint32_t *longw, const uint32_t *inw,
+                         uint32_t *vis, uint32_t *out, uint32_t *parent, int64_t *fb_ga)
+{
+    fb_ga[0] = fb_ga[1] = 0;
+    bu_multiple_set(rs, adj, n, (n + 31) / 32, max_pos, posw, longw, inw, vis, out, parent,
+                    &fb_ga[0], &fb_ga[1]);
+}
+
 static int64_t popcount_words(const uint32_t *w, int64_t nw)
 {
     int64_t s = 0;

@@ -55,6 +55,10 @@ def lib():
         L.hbo_bfs_reference.argtypes = [P, P, i64, i64, P, P]
         L.hbo_hybrid_bfs.restype = i64
         L.hbo_hybrid_bfs.argtypes = [P, P, i64, i64, i32, i32, i64, i64, i32, i32, i32, P, P, P, i64]
+        L.hbo_td_layer.restype = i64
+        L.hbo_td_layer.argtypes = [P, P, i64, P, P, P, P]
+        L.hbo_bu_layer.argtypes = [P, P, i64, P, P, P, P]
+        L.hbo_bu_multiple_set.argtypes = [P, P, i64, i32, P, P, P, P, P, P, P]
         L.hbo_validate_tree.restype = i32
         L.hbo_validate_tree.argtypes = [P, P, i64, i64, P, P]
         _lib = L
@@ -197,3 +201,23 @@ def minid_parents(g: HostCsr, levels: np.ndarray, source: int) -> np.ndarray:
     np.minimum.at(parent, src[ok], dst[ok].astype(np.uint64))
     parent[source] = source
     return parent.astype(np.uint32)
+
+
+# ---- per-layer steps (_native.pyx:65-239), in place on host arrays ----
+
+def td_layer(rs, adj, n, inw, vis, out, parent) -> int:
+    """top_down_layer / top_down_chunked (returns the chunked gather count)."""
+    return int(lib().hbo_td_layer(_p(rs), _p(adj), n, _p(inw), _p(vis), _p(out), _p(parent)))
+
+
+def bu_layer(rs, adj, n, inw, vis, out, parent) -> None:
+    """bottom_up_layer."""
+    lib().hbo_bu_layer(_p(rs), _p(adj), n, _p(inw), _p(vis), _p(out), _p(parent))
+
+
+def bu_multiple_set(rs, adj, n, max_pos, posw, longw, inw, vis, out, parent):
+    """bottom_up_multiple_set -> (fallback, gathers)."""
+    fg = np.zeros(2, dtype=np.int64)
+    lib().hbo_bu_multiple_set(_p(rs), _p(adj), n, max_pos, _p(posw), _p(longw), _p(inw), _p(vis),
+                              _p(out), _p(parent), _p(fg))
+    return int(fg[0]), int(fg[1])

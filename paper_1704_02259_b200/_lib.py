@@ -70,6 +70,9 @@ SIGNATURES = {
     "hbfs_phase_times": (C.c_int, [P, P, i64]),
     "hbfs_traversal_bytes_layers": (C.c_int, [P, i64, P, P, i64, P, P]),
     # multi-GPU partition (csrc/part.cu)
+    "hbfs_layer_top_down": (C.c_int, [P, P, P, P, P, P, i64, P, P]),
+    "hbfs_layer_bottom_up": (C.c_int, [P, P, P, P, P, P, i64, i32, P, P, P]),
+    "hbfs_reference_bfs": (C.c_int, [P, P, i64, i64, P, P, P]),
     "hbfs_part_build": (C.c_int, [P, P, i64, i64, i64, i64, C.c_int, C.c_int, P, C.POINTER(P)]),
     "hbfs_part_from_csr": (C.c_int, [P, P, i64, i64, i64, i64, P, C.POINTER(P)]),
     "hbfs_part_info": (C.c_int, [P, P, P, P, P, P]),

@@ -32,3 +32,18 @@ def resolve_engine(engine: str = "auto", backend: str = "simd") -> str:
     if engine not in ENGINES:
         raise ValueError(f"engine must be one of {ENGINES}")
     return "cuda"
+
+
+def bfs_reference(g, source: int, engine: str = "auto"):
+    """Oracle traversal (engine.py:158-170): the FIFO-queue BFS of
+    _native.bfs_reference on the GPU -> (BfsTree, levels int32[n]).  Parents
+    follow the queue's first-discoverer rule, not the min-id rule."""
+    from . import native
+    from .frontier import BfsTree
+
+    resolve_engine(engine)
+    n = g.num_vertices
+    if not 0 <= source < n:
+        raise IndexError(f"source {source} out of range [0, {n})")
+    parent, levels = native.bfs_reference(g.row_starts, g.adjacency, n, source)
+    return BfsTree(parent=parent, source=int(source)), levels
