@@ -146,6 +146,11 @@ int hbfs_traversal_bytes_layers(hbfs_graph *g, int64_t root, const int32_t *leve
  * 0 = phase not taken).  rows <= 1024. */
 int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows);
 
+/* Measurement only: GB/s of random 32-byte sector reads over a 2^log_bytes
+ * buffer, each warp's 32 lanes inside one random 2^log_region-byte region (the
+ * access pattern of the traversal's gathers; bench.py's second roofline). */
+int hbfs_probe_random_sectors(int log_bytes, int log_region, double *gbs);
+
 /* ---- per-layer steps on caller buffers: the hybfs._native surface ----
  * All pointers are DEVICE pointers in the reference's layout: rs int64[n+1],
  * adj uint32[arcs], LSB-first bitmaps uint32[ceil(n/32)] (frontier.py:3-6),
