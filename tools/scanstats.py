@@ -53,3 +53,9 @@ tl = (scan - lane_cov).clamp(min=0)[tail]
 print(f"tail rows {int(tail.sum())} ({100*float(tail.float().mean()):.1f}% of candidates)  tail entries {int(tl.sum())}")
 q = torch.quantile(tl.float()[:1 << 24], torch.tensor([0.5, 0.9, 0.99], device="cuda"))
 print(f"tail length p50/p90/p99 {q.tolist()}  steps of 128: {int(((tl + 127) // 128).sum())}")
+# entries probed per candidate, bucketed (where the layer's probe work sits)
+edges = [0, 4, 8, 16, 32, 128, 1024, 1 << 40]
+sc = scan
+for lo_, hi_ in zip(edges[:-1], edges[1:]):
+    msk = (sc > lo_) & (sc <= hi_)
+    print(f"  scan ({lo_:>5},{hi_ if hi_ < 1 << 40 else 'inf':>5}]: rows {int(msk.sum()):>10}  entries {int(sc[msk].sum()):>12}")
