@@ -5,9 +5,10 @@
 // replicated (n bits each); parent/level are owned-only.  Per layer the host
 // (paper_1704_02259_b200/mgpu.py) runs one of
 //   bottom-up:  hbfs_part_bu        -> next-frontier slice of the owned words
-//   top-down:   hbfs_part_td_expand -> per-owner queues of the unvisited
-//                                      targets, each once, with its min parent
-//                                      candidate; counts per owner
+//   top-down:   hbfs_part_td_expand -> min parent candidate per unvisited
+//                                      target + a touch bitmap (fire-and-
+//                                      forget reductions), scanned into
+//                                      record counts per owner
 //               [all-to-all of the counts]
 //               hbfs_part_td_pack   -> 8-byte (parent, vertex) records packed
 //                                      by owner
@@ -35,13 +36,15 @@ struct Part {
     DevBuf F, V;              // uint32[W] replicated
     DevBuf parent, level;     // owned
     DevBuf q;                 // uint32[nloc] owned frontier queue
+    DevBuf seg_u, seg_k;      // long-row segments (row, first arc), <= arcs/4096 + nloc/1024
     DevBuf scratch;           // counters etc.
     // top-down exchange state (all kept clean between layers)
     DevBuf cand;              // int32[n]  min parent candidate per target (INT32_MAX = none)
     DevBuf touch;             // uint32[W] target already queued this layer
     DevBuf candown;           // int32[nloc] min over the received records
-    DevBuf sendq;             // uint32[world * span] per-owner target queues
-    DevBuf scnt;              // uint64[world] per-owner queue fill
+    DevBuf wcnt, wexcl;       // uint32[W + 1] touch-word popcounts and their exclusive prefix
+    DevBuf scan_tmp;          // CUB scan scratch
+    size_t scan_bytes = 0;
     int world = 0;            // partition the queues were sized for
     int64_t span = 0;         // vertices per owner block (word aligned)
 };
@@ -203,76 +206,99 @@ __global__ void kp_bu(int64_t wloc, int64_t nloc, int64_t lo, int32_t depth1, in
     }
 }
 
-// owned frontier queue from the replicated F
-__global__ void kp_queue(int64_t wloc, int64_t lo, const uint32_t *F, uint32_t *q,
-                         unsigned long long *qn) {
+// Owned frontier queue from the replicated F.  Rows of >= kSegArcs arcs are
+// also cut into segments of kSegArcs arcs (one entry per segment), so a hub
+// row spreads over many CTAs instead of serialising one.
+constexpr int64_t kSegArcs = 4096;
+
+__global__ void kp_queue(int64_t wloc, int64_t lo, const uint32_t *F, const uint64_t *rs, uint32_t *q,
+                         unsigned long long *qn, uint32_t *seg_u, uint64_t *seg_k,
+                         unsigned long long *segn) {
     PSTRIDE(j, wloc) {
         uint32_t bits = F[(lo >> 5) + j];
         while (bits) {
             const int b = __ffs(bits) - 1;
             bits &= bits - 1;
-            q[atomicAdd(qn, 1ull)] = (uint32_t)(j * 32 + b);  // local id
+            const uint32_t ul = (uint32_t)(j * 32 + b);  // local id
+            q[atomicAdd(qn, 1ull)] = ul;
+            const uint64_t s = rs[ul], e = rs[ul + 1];
+            if (e - s >= 1024) {
+                const unsigned long long ns = (e - s + kSegArcs - 1) / kSegArcs;
+                const unsigned long long at = atomicAdd(segn, ns);
+                for (unsigned long long t = 0; t < ns; ++t) {
+                    seg_u[at + t] = ul;
+                    seg_k[at + t] = s + t * kSegArcs;
+                }
+            }
         }
     }
 }
 
-// Top-down expansion: warp per frontier row for short rows, the whole CTA for
-// rows of >= 1024 arcs.  Every arc into an unvisited target lowers cand[v];
-// the first arc to reach v this layer (touch bit) appends v to its owner's
-// queue, so each target is sent once per rank with its rank-local min parent.
+// Top-down expansion.  Every arc into an unvisited target lowers cand[v]
+// (atomicMin) and marks v in the touch bitmap (a reduction, no return): both
+// fire-and-forget.  The records are built afterwards by a scan of the touch
+// bitmap in vertex order, which is owner order (owner blocks are contiguous
+// word ranges), so no per-target append and no shared counter.
 __device__ __forceinline__ void td_arc(uint32_t v, int32_t u, const uint32_t *V, int32_t *cand,
-                                       uint32_t *touch, uint32_t *sendq, unsigned long long *scnt,
-                                       int64_t span) {
+                                       uint32_t *touch) {
     const uint32_t b = 1u << (v & 31);
-    if ((V[v >> 5] & b)) return;
+    if (V[v >> 5] & b) return;
     atomicMin(&cand[v], u);
-    if (__ldcg(&touch[v >> 5]) & b) return;
-    if (atomicOr(&touch[v >> 5], b) & b) return;
-    const int64_t o = (int64_t)v / span;
-    const unsigned long long i = atomicAdd(&scnt[o], 1ull);
-    sendq[o * span + (int64_t)i] = v;
+    if (!(__ldcg(&touch[v >> 5]) & b)) atomicOr(&touch[v >> 5], b);
 }
 
-__global__ void kp_td(const uint32_t *q, int64_t qn, int64_t lo, const uint64_t *rs,
+// Short rows (< 1024 arcs): warp per row; long rows: CTA per kSegArcs-arc
+// segment.  Counts are read on the device (no host round trip per layer).
+__global__ void kp_td(const uint32_t *q, const unsigned long long *qn_p, int64_t lo, const uint64_t *rs,
                       const uint32_t *adj, const uint32_t *V, int32_t *cand, uint32_t *touch,
-                      uint32_t *sendq, unsigned long long *scnt, int64_t span, int big) {
+                      const uint32_t *seg_u, const uint64_t *seg_k, const unsigned long long *segn_p) {
     const int lane = threadIdx.x & 31;
-    if (!big) {
-        for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
-             i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-            const uint32_t ul = q[i];
-            const uint64_t s = rs[ul], e = rs[ul + 1];
-            if (e - s >= 1024) continue;
-            const int32_t u = (int32_t)(lo + ul);
-            for (uint64_t k = s + lane; k < e; k += 32) td_arc(adj[k], u, V, cand, touch, sendq, scnt, span);
-        }
-    } else {
-        for (int64_t i = blockIdx.x; i < qn; i += gridDim.x) {
-            const uint32_t ul = q[i];
-            const uint64_t s = rs[ul], e = rs[ul + 1];
-            if (e - s < 1024) continue;
-            const int32_t u = (int32_t)(lo + ul);
-            for (uint64_t k = s + threadIdx.x; k < e; k += blockDim.x)
-                td_arc(adj[k], u, V, cand, touch, sendq, scnt, span);
-        }
+    const int64_t qn = (int64_t)*qn_p, segn = (int64_t)*segn_p;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t ul = q[i];
+        const uint64_t s = rs[ul], e = rs[ul + 1];
+        if (e - s >= 1024) continue;
+        const int32_t u = (int32_t)(lo + ul);
+        for (uint64_t k = s + lane; k < e; k += 32) td_arc(adj[k], u, V, cand, touch);
+    }
+    for (int64_t g = blockIdx.x; g < segn; g += gridDim.x) {
+        const uint32_t ul = seg_u[g];
+        const uint64_t k0 = seg_k[g], e = rs[ul + 1];
+        const uint64_t k1 = k0 + kSegArcs < e ? k0 + kSegArcs : e;
+        const int32_t u = (int32_t)(lo + ul);
+        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) td_arc(adj[k], u, V, cand, touch);
     }
 }
 
-// Records of the queued targets, packed by owner (record = parent << 32 | v);
-// resets cand and touch behind itself.
-__global__ void kp_td_pack(int world, int64_t span, const uint32_t *sendq,
-                           const unsigned long long *scnt, int32_t *cand, uint32_t *touch,
+__global__ void kp_touch_popc(int64_t W, const uint32_t *touch, uint32_t *cnt) {
+    PSTRIDE(w, W) cnt[w] = __popc(touch[w]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[W] = 0;
+}
+
+// Records per owner o = touched vertices in its word block [o*wper, (o+1)*wper).
+__global__ void kp_owner_counts(int world, int64_t wper, int64_t W, const uint32_t *excl, int64_t *counts) {
+    const int o = threadIdx.x;
+    if (o < world) {
+        const int64_t a = o * wper < W ? o * wper : W, b = (o + 1) * wper < W ? (o + 1) * wper : W;
+        counts[o] = (int64_t)excl[b] - (int64_t)excl[a];
+    }
+}
+
+// Records (parent << 32 | v) in vertex order = owner order, at the scanned
+// word offsets; resets cand and touch behind itself.
+__global__ void kp_td_pack(int64_t W, const uint32_t *excl, int32_t *cand, uint32_t *touch,
                            unsigned long long *rec) {
-    int64_t total = 0;
-    for (int o = 0; o < world; ++o) total += (int64_t)scnt[o];
-    PSTRIDE(k, total) {
-        int64_t base = 0;
-        int o = 0;
-        while (k - base >= (int64_t)scnt[o]) base += (int64_t)scnt[o++];
-        const uint32_t v = sendq[o * span + (k - base)];
-        rec[k] = ((unsigned long long)(uint32_t)cand[v] << 32) | v;
-        cand[v] = 0x7FFFFFFF;
-        touch[v >> 5] = 0u;
+    PSTRIDE(w, W) {
+        uint32_t bits = touch[w];
+        if (!bits) continue;
+        touch[w] = 0u;
+        unsigned long long pos = excl[w];
+        for (; bits; bits &= bits - 1) {
+            const uint32_t v = (uint32_t)(w * 32 + __ffs(bits) - 1);
+            rec[pos++] = ((unsigned long long)(uint32_t)cand[v] << 32) | v;
+            cand[v] = 0x7FFFFFFF;
+        }
     }
 }
 
@@ -331,8 +357,19 @@ static int part_alloc_state(Part *P) {
     HB_CHECK(P->level.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->q.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->scratch.alloc(64));
+    {
+        const int64_t nseg = P->arcs / kSegArcs + P->nloc / 1024 + 16;
+        HB_CHECK(P->seg_u.alloc(nseg * 4));
+        HB_CHECK(P->seg_k.alloc(nseg * 8));
+    }
     HB_CHECK(P->cand.alloc(P->n * 4 + 16));
     HB_CHECK(P->touch.alloc(P->W * 4 + 16));
+    HB_CHECK(P->wcnt.alloc((P->W + 1) * 4 + 16));
+    HB_CHECK(P->wexcl.alloc((P->W + 1) * 4 + 16));
+    P->scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, P->scan_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (int)(P->W + 1));
+    HB_CHECK(P->scan_tmp.alloc(P->scan_bytes + 16));
     HB_CHECK(P->candown.alloc(P->nloc * 4 + 16));
     kp_fill_i32<<<pgrid(P->n), 256>>>(P->cand.as<int32_t>(), P->n, 0x7FFFFFFF);
     kp_fill_i32<<<pgrid(P->nloc), 256>>>(P->candown.as<int32_t>(), P->nloc, 0x7FFFFFFF);
@@ -563,34 +600,23 @@ extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t world, int64_t *send_co
     const int64_t wper = (P->W + world - 1) / world;
     const int64_t span = wper * 32;
     if (P->world != world) {
-        HB_CHECK(P->sendq.alloc(world * span * 4 + 16));
-        HB_CHECK(P->scnt.alloc(world * 8 + 16));
         P->world = world;
         P->span = span;
     }
-    unsigned long long *scnt = P->scnt.as<unsigned long long>();
-    unsigned long long *qn = P->scratch.as<unsigned long long>();
-    HB_CUDA(cudaMemsetAsync(qn, 0, 8, st));
-    HB_CUDA(cudaMemsetAsync(scnt, 0, world * 8, st));
-    kp_queue<<<pgrid(P->wloc), 256, 0, st>>>(P->wloc, P->lo, P->F.as<uint32_t>(),
-                                             P->q.as<uint32_t>(), qn);
+    unsigned long long *qn = P->scratch.as<unsigned long long>();  // [0] queue, [1] segments
+    HB_CUDA(cudaMemsetAsync(qn, 0, 16, st));
+    kp_queue<<<pgrid(P->wloc), 256, 0, st>>>(P->wloc, P->lo, P->F.as<uint32_t>(), P->rs.as<uint64_t>(),
+                                             P->q.as<uint32_t>(), qn, P->seg_u.as<uint32_t>(),
+                                             P->seg_k.as<uint64_t>(), qn + 1);
+    kp_td<<<148 * 8, 256, 0, st>>>(P->q.as<uint32_t>(), qn, P->lo, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
+                                   P->V.as<uint32_t>(), P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
+                                   P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(), qn + 1);
+    uint32_t *cnt = P->wcnt.as<uint32_t>();
+    kp_touch_popc<<<pgrid(P->W + 1), 256, 0, st>>>(P->W, P->touch.as<uint32_t>(), cnt);
+    size_t tb = P->scan_bytes;
+    HB_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, tb, cnt, P->wexcl.as<uint32_t>(), (int)(P->W + 1), st));
+    kp_owner_counts<<<1, 32, 0, st>>>(world, wper, P->W, P->wexcl.as<uint32_t>(), send_counts);
     HB_CUDA(cudaGetLastError());
-    unsigned long long h = 0;
-    HB_CUDA(cudaMemcpyAsync(&h, qn, 8, cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaStreamSynchronize(st));
-    if (h > 0) {
-        kp_td<<<pgrid((int64_t)h * 32), 256, 0, st>>>(P->q.as<uint32_t>(), (int64_t)h, P->lo,
-                                                      P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-                                                      P->V.as<uint32_t>(), P->cand.as<int32_t>(),
-                                                      P->touch.as<uint32_t>(), P->sendq.as<uint32_t>(),
-                                                      scnt, span, 0);
-        kp_td<<<(int)std::min<int64_t>((int64_t)h, 148 * 8), 512, 0, st>>>(
-            P->q.as<uint32_t>(), (int64_t)h, P->lo, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-            P->V.as<uint32_t>(), P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
-            P->sendq.as<uint32_t>(), scnt, span, 1);
-        HB_CUDA(cudaGetLastError());
-    }
-    HB_CUDA(cudaMemcpyAsync(send_counts, scnt, world * 8, cudaMemcpyDeviceToDevice, st));
     return HBFS_OK;
     HB_ENTRY_END
 }
@@ -601,10 +627,9 @@ extern "C" int hbfs_part_td_pack(hbfs_part *P, uint64_t *records, void *stream) 
     HB_ENTRY_BEGIN
     if (!P || !records || P->world < 1) return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    kp_td_pack<<<pgrid(P->nloc), 256, 0, st>>>(P->world, P->span, P->sendq.as<uint32_t>(),
-                                               P->scnt.as<unsigned long long>(),
-                                               P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
-                                               reinterpret_cast<unsigned long long *>(records));
+    kp_td_pack<<<pgrid(P->W), 256, 0, st>>>(P->W, P->wexcl.as<uint32_t>(), P->cand.as<int32_t>(),
+                                            P->touch.as<uint32_t>(),
+                                            reinterpret_cast<unsigned long long *>(records));
     HB_CUDA(cudaGetLastError());
     return HBFS_OK;
     HB_ENTRY_END
