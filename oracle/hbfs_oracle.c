@@ -337,6 +337,25 @@ static void bu_multiple_set(const int64_t *rs, const uint32_t *adj, int64_t n, i
     }
 }
 
+/* The F1 rule: parent[v] = min{u in Adj(v) : level[u] = level[v] - 1}
+ * = the first such entry of v's sorted row; NIL for unreached, source for itself. */
+void hbo_minid_parents(const int64_t *rs, const uint32_t *adj, int64_t n, const int32_t *level,
+                       int64_t source, uint32_t *parent)
+{
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; ++v) {
+        uint32_t p = 0xFFFFFFFFu;
+        if (v == source) {
+            p = (uint32_t)source;
+        } else if (level[v] >= 1) {
+            const int32_t want = level[v] - 1;
+            for (int64_t k = rs[v]; k < rs[v + 1]; ++k)
+                if (level[adj[k]] == want) { p = adj[k]; break; }
+        }
+        parent[v] = p;
+    }
+}
+
 /* Exported per-layer steps (test checkers for csrc/layer.cu). */
 int64_t hbo_td_layer(const int64_t *rs, const uint32_t *adj, int64_t n, const uint32_t *inw,
                      uint32_t *vis, uint32_t *out, uint32_t *parent)

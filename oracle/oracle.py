@@ -55,6 +55,7 @@ def lib():
         L.hbo_bfs_reference.argtypes = [P, P, i64, i64, P, P]
         L.hbo_hybrid_bfs.restype = i64
         L.hbo_hybrid_bfs.argtypes = [P, P, i64, i64, i32, i32, i64, i64, i32, i32, i32, P, P, P, i64]
+        L.hbo_minid_parents.argtypes = [P, P, i64, P, i64, P]
         L.hbo_td_layer.restype = i64
         L.hbo_td_layer.argtypes = [P, P, i64, P, P, P, P]
         L.hbo_bu_layer.argtypes = [P, P, i64, P, P, P, P]
@@ -190,17 +191,13 @@ def validate_tree(g: HostCsr, source: int, parent: np.ndarray):
 
 
 def minid_parents(g: HostCsr, levels: np.ndarray, source: int) -> np.ndarray:
-    """The F1 rule: parent[v] = min{u in Adj(v): level u = level v - 1}."""
+    """The F1 rule (SURVEY §0): parent[v] = min{u in Adj(v): level u = level v - 1}
+    (the first such entry of the sorted row; C, OpenMP)."""
     n = g.num_vertices
-    deg = g.degrees()
-    src = np.repeat(np.arange(n, dtype=np.int64), deg)
-    dst = g.adjacency.astype(np.int64)
-    lv = levels.astype(np.int64)
-    ok = (lv[src] >= 1) & (lv[dst] == lv[src] - 1)
-    parent = np.full(n, NIL, dtype=np.uint64)
-    np.minimum.at(parent, src[ok], dst[ok].astype(np.uint64))
-    parent[source] = source
-    return parent.astype(np.uint32)
+    lv = np.ascontiguousarray(levels, dtype=np.int32)
+    parent = np.empty(n, dtype=np.uint32)
+    lib().hbo_minid_parents(_p(g.row_starts), _p(g.adjacency), n, _p(lv), int(source), _p(parent))
+    return parent
 
 
 # ---- per-layer steps (_native.pyx:65-239), in place on host arrays ----
