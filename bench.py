@@ -299,7 +299,9 @@ def run_ours(args, cfg):
             ts = sweep(tr)
             for i, t in enumerate(ts):
                 per_root[i].append(t)
-            launches += len(ts)
+            # per traversal: the persistent bfs_kernel, plus levels_kernel when
+            # levels are stamped from the depth planes (n >= 2^22, csrc/bfs.cu)
+            launches += len(ts) * (2 if n >= (1 << 22) else 1)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     total_dev = sum(sum(x) for x in per_root)
@@ -359,7 +361,7 @@ def run_ours(args, cfg):
         "wall_s_timed_region": wall,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "bfs_kernel (persistent, one launch per traversal)",
+                     "kernel": "bfs_kernel (persistent, one launch per traversal; + levels_kernel)",
                      "bytes_per_launch": b_sector / len(roots),
                      "useful_bytes_per_launch": b_useful / len(roots),
                      "launch_ms": t_roots / len(roots) * 1e3, "peak_source": peak_src,
