@@ -386,14 +386,15 @@ def run_ours(args, cfg):
 
 
 def run_distributed(args, cfg):
-    """N > 1: the 1D-partitioned traversal (paper_1704_02259_b200.mgpu) over NCCL,
-    one rank per GPU; per-root time = max over ranks of the CUDA-event time."""
+    """N > 1: the 1D-partitioned traversal (mgpu.NcclBfs: per-layer loop in C++
+    over NCCL), one rank per GPU; per-root time = max over ranks of the
+    CUDA-event time."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1704_02259_b200 as hb
-    from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, TorchComm
+    from paper_1704_02259_b200.mgpu import CudaRankOps, NcclBfs, TorchComm
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -402,7 +403,7 @@ def run_distributed(args, cfg):
     params = hb.GraphParams(scale=cfg["scale"], edgefactor=16, seed=1, probs=cfg["probs"])
     ops = CudaRankOps.generate(params, ws, rank, device=dev)
     comm = TorchComm()
-    db = DistBfs([ops], comm)
+    db = NcclBfs(ops, ws, rank)  # the per-layer loop in C++ over NCCL (csrc/part.cu hbfs_mg_bfs)
     # roots: identical on every rank (computed from the generator's graph on rank 0)
     roots_t = torch.zeros(ROOTS, dtype=torch.int64, device=dev)
     if rank == 0:
@@ -459,7 +460,7 @@ def run_distributed(args, cfg):
             "data": "synthetic (bit-exact reference R-MAT generator on device, seed 1)",
             "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
                        "roots": ROOTS, "heuristic": cfg["heur"], "parent_mode": "minid",
-                       "parallelism": f"1d-partition x{ws} (NCCL all-gather / all-to-all-v records / all-reduce)",
+                       "parallelism": f"1d-partition x{ws} (C++ loop; NCCL all-gather / send-recv records / all-reduce)",
                        "l2": "flushed (256 MB write) before every traversal"},
             "gpu_launches": None,
             "wall_s_timed_region": wall,

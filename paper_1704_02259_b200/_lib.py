@@ -86,6 +86,10 @@ SIGNATURES = {
     "hbfs_part_td_apply": (C.c_int, [P, i32, P, i64, P, P, P]),
     "hbfs_part_absorb": (C.c_int, [P, P, P]),
     "hbfs_part_outputs": (C.c_int, [P, P, P, C.c_int, P]),
+    "hbfs_nccl_unique_id": (C.c_int, [P, i64]),
+    "hbfs_mg_init": (C.c_int, [P, i32, i32, C.POINTER(P)]),
+    "hbfs_mg_free": (C.c_int, [P]),
+    "hbfs_mg_bfs": (C.c_int, [P, P, i64, C.POINTER(hbfs_params), P, i64, P, P, P]),
 }
 
 _lib = None

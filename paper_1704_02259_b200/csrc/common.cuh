@@ -73,6 +73,32 @@ struct DevBuf {
     T *as() const { return static_cast<T *>(p); }
 };
 
+struct Heur {
+    int heuristic, counter_mode, force;
+    int64_t alpha, beta, n;
+};
+
+// Direction rule: hybrid.py:62-80 (reference rule) or Beamer/GAP.  Host+device
+// so the controller is identical wherever it runs (persistent kernel, the
+// multi-GPU host loop).
+__host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64_t e_f,
+                                      int64_t eu_v, int64_t eu_e, int64_t prev_vf,
+                                      int64_t *fv, int64_t *gv) {
+    *gv = H.n / H.beta;
+    if (H.heuristic == HBFS_HEURISTIC_BEAMER) {
+        *fv = eu_e / H.alpha;
+        if (H.force >= 0) return H.force;
+        if (cur == HBFS_TOP_DOWN) return e_f > *fv ? HBFS_BOTTOM_UP : HBFS_TOP_DOWN;
+        return (v_f < prev_vf && v_f <= *gv) ? HBFS_TOP_DOWN : HBFS_BOTTOM_UP;
+    }
+    const int64_t e_u = H.counter_mode ? eu_e : eu_v;
+    *fv = e_u / H.alpha;
+    if (H.force >= 0) return H.force;
+    if (v_f > *fv) return HBFS_BOTTOM_UP;
+    if (v_f < *gv) return HBFS_TOP_DOWN;
+    return cur;
+}
+
 }  // namespace hbfs
 
 struct hbfs_graph {

@@ -679,3 +679,217 @@ extern "C" int hbfs_part_outputs(hbfs_part *P, uint32_t *parent, int32_t *level,
     return HBFS_OK;
     HB_ENTRY_END
 }
+
+// ------------------------------------------------------------------------
+// Multi-GPU traversal loop in C++ over NCCL: one process per GPU, the same
+// per-layer steps as mgpu.DistBfs (which keeps the host logic testable with
+// gloo on CPU) without Python in the loop.  Per layer: the rank's kernels,
+// in-place ncclAllGather of the next-frontier slices, ncclAllReduce of the
+// four counters, and on top-down layers grouped ncclSend/ncclRecv for the
+// per-owner counts and the 8-byte records.  Host round trips per layer: the
+// counter read for the direction decision (hybrid.py:123-173) and, on
+// top-down layers, the record counts (NCCL needs split sizes on the host).
+#include <nccl.h>
+
+#include <vector>
+
+#define HB_NCCL(expr)                                                                       \
+    do {                                                                                    \
+        ncclResult_t r_ = (expr);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return ::hbfs::set_error(HBFS_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr, \
+                                     ncclGetErrorString(r_));                               \
+    } while (0)
+
+struct hbfs_mg {
+    ncclComm_t comm = nullptr;
+    int world = 0, rank = 0;
+    hbfs::DevBuf next_full, ctr, counts, recs_s, recs_r, scal;
+    size_t cap_s = 0, cap_r = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ~hbfs_mg() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (comm) ncclCommDestroy(comm);
+    }
+};
+
+extern "C" int hbfs_nccl_unique_id(void *out, int64_t bytes) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!out || bytes < (int64_t)sizeof(ncclUniqueId)) return set_error(HBFS_EINVAL, "need %d bytes", (int)sizeof(ncclUniqueId));
+    ncclUniqueId id;
+    HB_NCCL(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_mg_init(const void *unique_id, int32_t world, int32_t rank, hbfs_mg **out) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!unique_id || !out || world < 1 || rank < 0 || rank >= world) return set_error(HBFS_EINVAL, "bad arguments");
+    hbfs_mg *M = new hbfs_mg();
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&M->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        M->comm = nullptr;
+        delete M;
+        return set_error(HBFS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    M->world = world;
+    M->rank = rank;
+    int rc = M->ctr.alloc(64);
+    if (!rc) rc = M->counts.alloc(16 * world + 16);
+    if (!rc) rc = M->scal.alloc(64);
+    if (!rc && (cudaEventCreate(&M->ev0) != cudaSuccess || cudaEventCreate(&M->ev1) != cudaSuccess))
+        rc = set_error(HBFS_ECUDA, "cudaEventCreate failed");
+    if (rc) {
+        delete M;
+        return rc;
+    }
+    *out = M;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+extern "C" int hbfs_mg_free(hbfs_mg *M) {
+    HB_ENTRY_BEGIN
+    delete M;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+namespace {
+int grow(hbfs::DevBuf &b, size_t &cap, size_t need) {
+    if (need <= cap) return HBFS_OK;
+    size_t c = std::max<size_t>(need + need / 4, 1 << 16);
+    HB_CHECK(b.alloc(c * 8));
+    cap = c;
+    return HBFS_OK;
+}
+}  // namespace
+
+extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_params *p,
+                           hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers,
+                           float *device_ms, void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!M || !P || !p) return set_error(HBFS_EINVAL, "null argument");
+    if (root < 0 || root >= P->n)
+        return set_error(HBFS_ERANGE, "source %lld out of range [0, %lld)", (long long)root, (long long)P->n);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int world = M->world, rank = M->rank;
+    const int64_t wper = (P->W + world - 1) / world;
+    if (P->lo != rank * wper * 32) return set_error(HBFS_EINVAL, "partition does not match rank/world");
+    if (!M->next_full.p || M->next_full.bytes < (size_t)(wper * world * 4))
+        HB_CHECK(M->next_full.alloc(wper * world * 4 + 16));
+    uint32_t *next_full = M->next_full.as<uint32_t>();
+    uint32_t *slice = next_full + rank * wper;
+    unsigned long long *ctr = M->ctr.as<unsigned long long>();
+    int64_t *sc = M->counts.as<int64_t>(), *rcv = sc + world;
+    int64_t *scal = M->scal.as<int64_t>();
+    Heur H;
+    H.heuristic = p->heuristic;
+    H.counter_mode = p->counter_mode;
+    H.force = p->force_direction;
+    H.alpha = p->alpha;
+    H.beta = p->beta;
+    H.n = P->n;
+
+    HB_CUDA(cudaEventRecord(M->ev0, st));
+    HB_CHECK(hbfs_part_init(P, root, st));
+    // root degree and the global arc count: one all-reduce
+    int64_t h2[2] = {0, P->arcs};
+    if (root >= P->lo && root < P->hi) HB_CHECK(hbfs_part_degree(P, root, &h2[0]));
+    HB_CUDA(cudaMemcpyAsync(scal, h2, 16, cudaMemcpyHostToDevice, st));
+    HB_NCCL(ncclAllReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
+    HB_CUDA(cudaMemcpyAsync(h2, scal, 16, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    const int64_t rdeg = h2[0], arcs_global = h2[1];
+    int64_t v_f = 1, e_f = rdeg, eu_v = P->n - 1, eu_e = arcs_global - rdeg, prev_vf = 0;
+    int cur = HBFS_TOP_DOWN;
+    int64_t layer = 0;
+    std::vector<int64_t> hc(2 * world);
+    while (v_f > 0) {
+        int64_t fv, gv;
+        const int d = decide(H, cur, v_f, e_f, eu_v, eu_e, prev_vf, &fv, &gv);
+        HB_CUDA(cudaMemsetAsync(slice, 0, wper * 4, st));
+        if (d == HBFS_BOTTOM_UP) {
+            HB_CHECK(hbfs_part_bu(P, (int32_t)layer, p->max_pos, slice, ctr, st));
+        } else {
+            HB_CHECK(hbfs_part_td_expand(P, world, sc, st));
+            HB_NCCL(ncclGroupStart());
+            for (int r = 0; r < world; ++r) {
+                HB_NCCL(ncclSend(sc + r, 1, ncclInt64, r, M->comm, st));
+                HB_NCCL(ncclRecv(rcv + r, 1, ncclInt64, r, M->comm, st));
+            }
+            HB_NCCL(ncclGroupEnd());
+            HB_CUDA(cudaMemcpyAsync(hc.data(), sc, 16 * world, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+            int64_t ns = 0, nr = 0;
+            for (int r = 0; r < world; ++r) {
+                ns += hc[r];
+                nr += hc[world + r];
+            }
+            HB_CHECK(grow(M->recs_s, M->cap_s, (size_t)ns));
+            HB_CHECK(grow(M->recs_r, M->cap_r, (size_t)nr));
+            HB_CHECK(hbfs_part_td_pack(P, M->recs_s.as<uint64_t>(), st));
+            uint64_t *rs_ = M->recs_s.as<uint64_t>(), *rr_ = M->recs_r.as<uint64_t>();
+            HB_NCCL(ncclGroupStart());
+            {
+                int64_t os = 0, orr = 0;
+                for (int r = 0; r < world; ++r) {
+                    if (hc[r]) HB_NCCL(ncclSend(rs_ + os, (size_t)hc[r], ncclUint64, r, M->comm, st));
+                    if (hc[world + r]) HB_NCCL(ncclRecv(rr_ + orr, (size_t)hc[world + r], ncclUint64, r, M->comm, st));
+                    os += hc[r];
+                    orr += hc[world + r];
+                }
+            }
+            HB_NCCL(ncclGroupEnd());
+            HB_CHECK(hbfs_part_td_apply(P, (int32_t)layer, rr_, nr, slice, ctr, st));
+        }
+        HB_NCCL(ncclAllGather(slice, next_full, (size_t)wper, ncclUint32, M->comm, st));
+        HB_NCCL(ncclAllReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
+        HB_CHECK(hbfs_part_absorb(P, next_full, st));
+        unsigned long long c4[4];
+        HB_CUDA(cudaMemcpyAsync(c4, ctr, 32, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        const int64_t nvf = (int64_t)c4[0], nef = (int64_t)c4[1];
+        if (trace && layer < trace_cap) {
+            hbfs_layer_row &r = trace[layer];
+            r.layer = (int32_t)(layer + 1);
+            r.direction = d;
+            r.v_f = v_f;
+            r.e_f = e_f;
+            r.e_u = p->counter_mode ? eu_e : eu_v;
+            r.f_value = fv;
+            r.g_value = gv;
+            if (!p->use_simd) {
+                r.fallback_count = 0;
+                r.gather_count = 0;
+            } else if (d == HBFS_TOP_DOWN) {
+                r.fallback_count = 0;
+                r.gather_count = e_f;
+            } else {
+                r.fallback_count = (int64_t)c4[3];
+                r.gather_count = (int64_t)c4[2];
+            }
+            r.elapsed = 0.0;
+        }
+        prev_vf = v_f;
+        v_f = nvf;
+        e_f = nef;
+        eu_v -= nvf;
+        eu_e -= nef;
+        cur = d;
+        ++layer;
+    }
+    HB_CUDA(cudaEventRecord(M->ev1, st));
+    HB_CUDA(cudaEventSynchronize(M->ev1));
+    if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, M->ev0, M->ev1));
+    if (n_layers) *n_layers = layer;
+    return HBFS_OK;
+    HB_ENTRY_END
+}

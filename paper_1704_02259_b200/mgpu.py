@@ -398,3 +398,68 @@ class DistBfs:
     def outputs(self):
         """Owned (parent, level) of each local rank, in rank order."""
         return [r.outputs() for r in self.ranks]
+
+
+# ------------------------------------------------ C++ loop over NCCL (GPUs)
+
+class NcclBfs:
+    """The per-layer loop of DistBfs in C++ over NCCL (csrc/part.cu
+    ``hbfs_mg_bfs``): same steps, same trace, no Python per layer.  One process
+    per GPU; the NCCL unique id goes from rank 0 to the others through the
+    caller's torch.distributed group (any backend)."""
+
+    def __init__(self, ops: CudaRankOps, world: int, rank: int, group=None):
+        from . import _lib
+
+        self._lib = _lib
+        self.ops = ops
+        self.lib = ops.lib
+        self.world, self.rank = world, rank
+        self.n = ops.n
+        idbuf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(self.lib.hbfs_nccl_unique_id(idbuf, 128))
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            dev = ops.device if dist.get_backend(group) == "nccl" else "cpu"
+            t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, 0, group=group)
+            idbuf = (C.c_uint8 * 128)(*t.cpu().tolist())
+        self.h = C.c_void_p()
+        _lib.check(self.lib.hbfs_mg_init(idbuf, world, rank, C.byref(self.h)))
+        self._rows = (_lib.hbfs_layer_row * 4096)()
+
+    def free(self):
+        if self.h:
+            self.lib.hbfs_mg_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def bfs(self, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = None,
+            use_simd: bool = True, force_direction=None) -> DistResult:
+        from .hybrid import _params
+
+        p = p if p is not None else HeuristicParams()
+        cfg = cfg if cfg is not None else VecConfig()
+        hp = _params(p, cfg, use_simd, force_direction, "minid")
+        nl, ms = C.c_int64(), C.c_float()
+        self._lib.check(self.lib.hbfs_mg_bfs(self.h, self.ops.h, int(root), C.byref(hp), self._rows,
+                                             len(self._rows), C.byref(nl), C.byref(ms),
+                                             self._lib.current_stream()))
+        kern = "simd" if use_simd else "scalar"
+        trace = [LayerTraceRow(layer=r.layer, direction=BOTTOM_UP if r.direction else TOP_DOWN, kernel=kern,
+                               v_f=r.v_f, e_f=r.e_f, e_u=r.e_u, f_value=r.f_value, g_value=r.g_value,
+                               elapsed=r.elapsed, fallback_count=r.fallback_count,
+                               gather_count=r.gather_count)
+                 for r in self._rows[: min(nl.value, len(self._rows))]]
+        return DistResult(trace=trace, seconds=ms.value * 1e-3)
+
+    def outputs(self):
+        return [self.ops.outputs()]

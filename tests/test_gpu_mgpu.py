@@ -65,3 +65,25 @@ def test_partitioned_generate_matches_single_gpu(cuda):
             assert np.array_equal(np.concatenate([o[1] for o in outs]), ref.level)
             assert np.array_equal(np.concatenate([o[0] for o in outs]), ref.parent)
             assert [r.direction for r in res.trace] == [r.direction for r in ref.trace]
+
+
+@pytest.mark.parametrize("name", ["k8", "k10", "u12"])
+def test_nccl_loop_single_rank(cuda, small_golden, name):
+    """The C++ per-layer loop over NCCL (hbfs_mg_bfs) at world size 1: same
+    levels, parents and trace as the reference in every mode."""
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, NcclBfs
+
+    rs, adj = small_golden[f"{name}/rs"], small_golden[f"{name}/adj"]
+    ops = CudaRankOps.from_csr(rs, adj, len(adj) // 2, 1, 0)
+    nb = NcclBfs(ops, 1, 0)
+    for s in small_golden[f"{name}/sources"][:4]:
+        s = int(s)
+        for mode, kw in MODES.items():
+            p = hb.HeuristicParams(**kw.get("p", {}))
+            res = nb.bfs(s, p, use_simd=kw["use_simd"], force_direction=kw.get("force_direction"))
+            par, lev = nb.outputs()[0]
+            assert np.array_equal(lev, small_golden[f"{name}/{s}/level"]), (name, s, mode)
+            assert np.array_equal(par, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
+            assert np.array_equal(trace_array(res.trace), small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)
+    nb.free()

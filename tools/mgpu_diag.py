@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_1704_02259_b200 as hb
-from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm
+from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm, NcclBfs
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
@@ -48,3 +48,20 @@ for P in [int(x) for x in a.ranks.split(",")]:
           f"mean {np.mean(ts) * 1e3:.3f} ms per root = {np.mean(ts) / P * 1e3:.3f} ms per rank-share")
     for r in ranks:
         r.free()
+
+# the C++ loop over NCCL, one rank (the per-layer host cost without Python)
+ops = CudaRankOps.generate(params, 1, 0)
+nb = NcclBfs(ops, 1, 0)
+nb.bfs(int(roots[0]), p)
+ts = []
+for s in roots:
+    res = nb.bfs(int(s), p)
+    ts.append(res.seconds)
+    if s == roots[0] and a.layers:
+        print("   layers: " + " ".join(f"{'B' if x.direction == 'bottom-up' else 'T'}{x.v_f}" for x in res.trace))
+    if int(s) in ref:
+        par, lev = nb.outputs()[0]
+        assert np.array_equal(lev, ref[int(s)].level) and np.array_equal(par, ref[int(s)].parent), "mismatch"
+print(f"NCCL C++ loop, world 1: hmean {len(ts) * m / sum(ts) / 1e9:.2f} GTEPS, mean {np.mean(ts) * 1e3:.3f} ms per root")
+nb.free()
+ops.free()
