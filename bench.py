@@ -470,6 +470,7 @@ def run_distributed(args, cfg):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    db.free()
     dist.destroy_process_group()
     return 0
 

@@ -91,7 +91,32 @@ def _ptr(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr())
 
 
-def _layer_buffers(rs, adj, inw, visw, outw, parent):
+def _size(x) -> int:
+    return int(x.numel()) if _is_tensor(x) else int(np.asarray(x).size)
+
+
+def _check_sizes(rs, inw, visw, outw, parent, n: int, adj=None) -> None:
+    """The Cython kernels trust their buffers; the device kernels must not
+    read or write past them, so the lengths the loops touch are checked."""
+    n = int(n)
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    nw = (n + 31) // 32
+    if _size(rs) < n + 1:
+        raise ValueError(f"rs has {_size(rs)} entries, needs n + 1 = {n + 1}")
+    for name, x in (("inw", inw), ("visw", visw), ("outw", outw)):
+        if _size(x) < nw:
+            raise ValueError(f"{name} has {_size(x)} words, needs ceil(n/32) = {nw}")
+    if _size(parent) < n:
+        raise ValueError(f"parent has {_size(parent)} entries, needs n = {n}")
+    if adj is not None and n > 0:
+        arcs = int(rs[n].item()) if _is_tensor(rs) else int(np.asarray(rs)[n])
+        if _size(adj) < arcs:
+            raise ValueError(f"adj has {_size(adj)} entries, rs[n] = {arcs}")
+
+
+def _layer_buffers(rs, adj, inw, visw, outw, parent, n):
+    _check_sizes(rs, inw, visw, outw, parent, n, adj)
     lib = _lib.load(require_device=True)
     bufs = [_dev(rs, "i64", "rs", False), _dev(adj, "u32", "adj", False), _dev(inw, "u32", "inw", False),
             _dev(visw, "u32", "visw", True), _dev(outw, "u32", "outw", True),
@@ -111,7 +136,7 @@ def top_down_layer(rs, adj, inw, visw, outw, parent, n: int) -> None:
 
 def top_down_chunked(rs, adj, inw, visw, outw, parent, n: int) -> int:
     """Chunked top-down layer; returns gather_count (_native.pyx:207-239)."""
-    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent)
+    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent, n)
     g = C.c_int64()
     _lib.check(lib.hbfs_layer_top_down(*(_ptr(t) for t, _ in b), int(n), C.byref(g),
                                        _lib.current_stream()))
@@ -121,7 +146,7 @@ def top_down_chunked(rs, adj, inw, visw, outw, parent, n: int) -> int:
 
 def bottom_up_layer(rs, adj, inw, visw, outw, parent, n: int) -> None:
     """Scalar bottom-up layer: masked full scan of all vertices (_native.pyx:89-104)."""
-    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent)
+    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent, n)
     _lib.check(lib.hbfs_layer_bottom_up(*(_ptr(t) for t, _ in b), int(n), 1, None, None,
                                         _lib.current_stream()))
     _finish(b)
@@ -146,7 +171,7 @@ def bottom_up_multiple_set(rs, adj, inw, visw, outw, parent, n: int, max_pos: in
             return 0, 0
     elif np.asarray(adj).size == 0:
         return 0, 0
-    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent)
+    lib, b = _layer_buffers(rs, adj, inw, visw, outw, parent, n)
     fb, ga = C.c_int64(), C.c_int64()
     _lib.check(lib.hbfs_layer_bottom_up(*(_ptr(t) for t, _ in b), int(n), int(max_pos), C.byref(fb),
                                         C.byref(ga), _lib.current_stream()))
@@ -157,6 +182,12 @@ def bottom_up_multiple_set(rs, adj, inw, visw, outw, parent, n: int, max_pos: in
 def bfs_reference(rs, adj, n: int, source: int):
     """Sequential queue-based BFS; returns (parent uint32[n], levels int32[n])
     (_native.pyx:39-62): levels, and the FIFO queue's first-discoverer parents."""
+    n = int(n)
+    if n <= 0 or _size(rs) < n + 1:
+        raise ValueError("rs must hold n + 1 >= 2 row starts")
+    arcs = int(rs[n].item()) if _is_tensor(rs) else int(np.asarray(rs)[n])
+    if _size(adj) < arcs:
+        raise ValueError(f"adj has {_size(adj)} entries, rs[n] = {arcs}")
     lib = _lib.load(require_device=True)
     torch = _torch()
     trs, _ = _dev(rs, "i64", "rs", False)
