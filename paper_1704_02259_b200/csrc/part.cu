@@ -689,16 +689,66 @@ extern "C" int hbfs_part_outputs(hbfs_part *P, uint32_t *parent, int32_t *level,
 // per-owner counts and the 8-byte records.  Host round trips per layer: the
 // counter read for the direction decision (hybrid.py:123-173) and, on
 // top-down layers, the record counts (NCCL needs split sizes on the host).
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <vector>
+
+// NCCL is resolved at first use (dlopen by SONAME), not linked: the process
+// may already hold torch's libnccl.so.2, and a second, older copy loaded first
+// by this library would shadow the symbols torch needs.  Python callers import
+// torch (and let it load its NCCL) before the first multi-GPU call.
+namespace {
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGetErrorString) getErrorString = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    bool ok = false;
+};
+
+const NcclApi &nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+#define HB_SYM(field, name) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, #name))
+        HB_SYM(getUniqueId, ncclGetUniqueId);
+        HB_SYM(commInitRank, ncclCommInitRank);
+        HB_SYM(commDestroy, ncclCommDestroy);
+        HB_SYM(getErrorString, ncclGetErrorString);
+        HB_SYM(groupStart, ncclGroupStart);
+        HB_SYM(groupEnd, ncclGroupEnd);
+        HB_SYM(send, ncclSend);
+        HB_SYM(recv, ncclRecv);
+        HB_SYM(allGather, ncclAllGather);
+        HB_SYM(allReduce, ncclAllReduce);
+#undef HB_SYM
+        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.getErrorString && a.groupStart &&
+               a.groupEnd && a.send && a.recv && a.allGather && a.allReduce;
+        return a;
+    }();
+    return api;
+}
+}  // namespace
 
 #define HB_NCCL(expr)                                                                       \
     do {                                                                                    \
         ncclResult_t r_ = (expr);                                                           \
         if (r_ != ncclSuccess)                                                              \
             return ::hbfs::set_error(HBFS_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr, \
-                                     ncclGetErrorString(r_));                               \
+                                     nccl().getErrorString(r_));                            \
+    } while (0)
+#define HB_NCCL_API()                                                                        \
+    do {                                                                                     \
+        if (!nccl().ok) return ::hbfs::set_error(HBFS_ENCCL, "libnccl.so.2 not loadable");   \
     } while (0)
 
 struct hbfs_mg {
@@ -710,7 +760,7 @@ struct hbfs_mg {
     ~hbfs_mg() {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
-        if (comm) ncclCommDestroy(comm);
+        if (comm) nccl().commDestroy(comm);
     }
 };
 
@@ -718,8 +768,9 @@ extern "C" int hbfs_nccl_unique_id(void *out, int64_t bytes) {
     HB_ENTRY_BEGIN
     clear_error();
     if (!out || bytes < (int64_t)sizeof(ncclUniqueId)) return set_error(HBFS_EINVAL, "need %d bytes", (int)sizeof(ncclUniqueId));
+    HB_NCCL_API();
     ncclUniqueId id;
-    HB_NCCL(ncclGetUniqueId(&id));
+    HB_NCCL(nccl().getUniqueId(&id));
     memcpy(out, &id, sizeof(id));
     return HBFS_OK;
     HB_ENTRY_END
@@ -729,14 +780,15 @@ extern "C" int hbfs_mg_init(const void *unique_id, int32_t world, int32_t rank, 
     HB_ENTRY_BEGIN
     clear_error();
     if (!unique_id || !out || world < 1 || rank < 0 || rank >= world) return set_error(HBFS_EINVAL, "bad arguments");
+    HB_NCCL_API();
     hbfs_mg *M = new hbfs_mg();
     ncclUniqueId id;
     memcpy(&id, unique_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&M->comm, world, id, rank);
+    ncclResult_t r = nccl().commInitRank(&M->comm, world, id, rank);
     if (r != ncclSuccess) {
         M->comm = nullptr;
         delete M;
-        return set_error(HBFS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        return set_error(HBFS_ENCCL, "ncclCommInitRank: %s", nccl().getErrorString(r));
     }
     M->world = world;
     M->rank = rank;
@@ -804,7 +856,7 @@ extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_pa
     int64_t h2[2] = {0, P->arcs};
     if (root >= P->lo && root < P->hi) HB_CHECK(hbfs_part_degree(P, root, &h2[0]));
     HB_CUDA(cudaMemcpyAsync(scal, h2, 16, cudaMemcpyHostToDevice, st));
-    HB_NCCL(ncclAllReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
+    HB_NCCL(nccl().allReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
     HB_CUDA(cudaMemcpyAsync(h2, scal, 16, cudaMemcpyDeviceToHost, st));
     HB_CUDA(cudaStreamSynchronize(st));
     const int64_t rdeg = h2[0], arcs_global = h2[1];
@@ -820,12 +872,12 @@ extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_pa
             HB_CHECK(hbfs_part_bu(P, (int32_t)layer, p->max_pos, slice, ctr, st));
         } else {
             HB_CHECK(hbfs_part_td_expand(P, world, sc, st));
-            HB_NCCL(ncclGroupStart());
+            HB_NCCL(nccl().groupStart());
             for (int r = 0; r < world; ++r) {
-                HB_NCCL(ncclSend(sc + r, 1, ncclInt64, r, M->comm, st));
-                HB_NCCL(ncclRecv(rcv + r, 1, ncclInt64, r, M->comm, st));
+                HB_NCCL(nccl().send(sc + r, 1, ncclInt64, r, M->comm, st));
+                HB_NCCL(nccl().recv(rcv + r, 1, ncclInt64, r, M->comm, st));
             }
-            HB_NCCL(ncclGroupEnd());
+            HB_NCCL(nccl().groupEnd());
             HB_CUDA(cudaMemcpyAsync(hc.data(), sc, 16 * world, cudaMemcpyDeviceToHost, st));
             HB_CUDA(cudaStreamSynchronize(st));
             int64_t ns = 0, nr = 0;
@@ -837,21 +889,21 @@ extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_pa
             HB_CHECK(grow(M->recs_r, M->cap_r, (size_t)nr));
             HB_CHECK(hbfs_part_td_pack(P, M->recs_s.as<uint64_t>(), st));
             uint64_t *rs_ = M->recs_s.as<uint64_t>(), *rr_ = M->recs_r.as<uint64_t>();
-            HB_NCCL(ncclGroupStart());
+            HB_NCCL(nccl().groupStart());
             {
                 int64_t os = 0, orr = 0;
                 for (int r = 0; r < world; ++r) {
-                    if (hc[r]) HB_NCCL(ncclSend(rs_ + os, (size_t)hc[r], ncclUint64, r, M->comm, st));
-                    if (hc[world + r]) HB_NCCL(ncclRecv(rr_ + orr, (size_t)hc[world + r], ncclUint64, r, M->comm, st));
+                    if (hc[r]) HB_NCCL(nccl().send(rs_ + os, (size_t)hc[r], ncclUint64, r, M->comm, st));
+                    if (hc[world + r]) HB_NCCL(nccl().recv(rr_ + orr, (size_t)hc[world + r], ncclUint64, r, M->comm, st));
                     os += hc[r];
                     orr += hc[world + r];
                 }
             }
-            HB_NCCL(ncclGroupEnd());
+            HB_NCCL(nccl().groupEnd());
             HB_CHECK(hbfs_part_td_apply(P, (int32_t)layer, rr_, nr, slice, ctr, st));
         }
-        HB_NCCL(ncclAllGather(slice, next_full, (size_t)wper, ncclUint32, M->comm, st));
-        HB_NCCL(ncclAllReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
+        HB_NCCL(nccl().allGather(slice, next_full, (size_t)wper, ncclUint32, M->comm, st));
+        HB_NCCL(nccl().allReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
         HB_CHECK(hbfs_part_absorb(P, next_full, st));
         unsigned long long c4[4];
         HB_CUDA(cudaMemcpyAsync(c4, ctr, 32, cudaMemcpyDeviceToHost, st));

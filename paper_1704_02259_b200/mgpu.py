@@ -409,6 +409,8 @@ class NcclBfs:
     caller's torch.distributed group (any backend)."""
 
     def __init__(self, ops: CudaRankOps, world: int, rank: int, group=None):
+        import torch  # noqa: F401  (loads torch's libnccl.so.2, which libhbfs then resolves)
+
         from . import _lib
 
         self._lib = _lib
@@ -463,3 +465,73 @@ class NcclBfs:
 
     def outputs(self):
         return [self.ops.outputs()]
+
+
+def run_benchmark_distributed(params, mode: str = "simd-hybrid", heuristic: HeuristicParams | None = None,
+                              cfg: VecConfig | None = None, runs: int = 64, allow_isolated: bool = False,
+                              source_seed: int | None = None, validate: bool = True):
+    """harness.run_benchmark over the 1D partition, one process per GPU
+    (torch.distributed initialised with NCCL): rank 0 samples the roots on
+    the full graph, every rank traverses its share through NcclBfs, per-root
+    time = max over ranks of the device time; trees are all-gathered and
+    validated on rank 0 with the device validator.  Returns the
+    BenchmarkReport on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    from .csr import generate_graph
+    from .harness import (BenchmarkReport, RunResult, _mode_args, harmonic_mean, sample_sources, teps,
+                          validate_tree)
+
+    heuristic = heuristic if heuristic is not None else HeuristicParams()
+    cfg = cfg if cfg is not None else VecConfig()
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    force, use_simd = _mode_args(mode)
+    g = None
+    roots_t = torch.zeros(runs, dtype=torch.int64, device=dev)
+    if rank == 0:
+        g = generate_graph(params)
+        seed = params.seed if source_seed is None else source_seed
+        roots_t.copy_(torch.from_numpy(sample_sources(g, runs, seed, allow_isolated=allow_isolated)
+                                       .astype(np.int64)))
+        if not validate:
+            g.free()
+            g = None
+    dist.broadcast(roots_t, 0)
+    ops = CudaRankOps.generate(params, ws, rank, device=dev)
+    nb = NcclBfs(ops, ws, rank)
+    n, m = params.num_vertices, params.num_edges
+    _, _, wper = partition(n, ws, 0)
+    results = []
+    for s in roots_t.tolist():
+        r = nb.bfs(int(s), heuristic, cfg, use_simd=use_simd, force_direction=force)
+        t = torch.tensor([r.seconds], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        par, lev = nb.outputs()[0]
+        pad = wper * 32
+        loc = torch.full((2, pad), -1, dtype=torch.int32, device=dev)
+        loc[0, : len(par)] = torch.from_numpy(par.view(np.int32)).to(dev)
+        loc[1, : len(lev)] = torch.from_numpy(lev).to(dev)
+        full = torch.empty((ws, 2, pad), dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(full, loc)
+        if rank == 0:
+            parent = full[:, 0, :].reshape(-1)[:n].contiguous()
+            level = full[:, 1, :].reshape(-1)[:n].contiguous()
+            traversed = int((level >= 0).sum().item()) - 1
+            secs = float(t.item())
+            ok = bool(validate_tree(g, int(s), parent, level)) if validate else True
+            results.append(RunResult(source=int(s), seconds=secs, teps=teps(m, secs) if traversed > 0 else 0.0,
+                                     valid=ok, trace=r.trace))
+    nb.free()
+    ops.free()
+    if rank != 0:
+        return None
+    if g is not None:
+        g.free()
+    positive = [r.teps for r in results if r.teps > 0]
+    secs = [r.seconds for r in results]
+    return BenchmarkReport(params=params, mode=mode, runs=results,
+                           harmonic_mean_teps=harmonic_mean(positive) if positive else 0.0,
+                           min_seconds=min(secs), max_seconds=max(secs), mean_seconds=sum(secs) / len(secs),
+                           zero_teps_runs=len(results) - len(positive), teps_denominator=m)

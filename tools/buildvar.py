@@ -25,7 +25,7 @@ def main(bfs_src, out):
         procs.append(subprocess.Popen(cmd))
     for p in procs:
         assert p.wait() == 0
-    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", out, *objs, "-lcudart_static", "-lnccl", "-ldl", "-lrt", "-lpthread"], check=True)
+    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", out, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"], check=True)
     print(out)
 
 
