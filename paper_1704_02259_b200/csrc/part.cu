@@ -37,6 +37,9 @@ struct Part {
     DevBuf parent, level;     // owned
     DevBuf q;                 // uint32[nloc] owned frontier queue
     DevBuf seg_u, seg_k;      // long-row segments (row, first arc), <= arcs/4096 + nloc/1024
+    DevBuf pieces, rcnt;      // range-ordered pieces (Piece); per-range counts/cursors
+    int64_t nseg_cap = 0;
+    int ranges = 1;
     DevBuf scratch;           // counters etc.
     // top-down exchange state (all kept clean between layers)
     DevBuf cand;              // int32[n]  min parent candidate per target (INT32_MAX = none)
@@ -234,6 +237,79 @@ __global__ void kp_queue(int64_t wloc, int64_t lo, const uint32_t *F, const uint
     }
 }
 
+// Column blocking of the long-row segments: a segment's targets are sorted, so
+// it splits into pieces by target range (2^kRangeBits vertices, 16 MB of
+// cand); pieces are ordered by range, so the CTAs working at any moment update
+// one or two L2-resident slices of cand/touch instead of the whole array.
+constexpr int kRangeBits = 22;
+
+__device__ __forceinline__ void seg_bounds(const uint32_t *seg_u, const uint64_t *seg_k, const uint64_t *rs,
+                                           int64_t g, uint32_t &ul, uint64_t &k0, uint64_t &k1) {
+    ul = seg_u[g];
+    k0 = seg_k[g];
+    const uint64_t e = rs[ul + 1];
+    k1 = k0 + kSegArcs < e ? k0 + kSegArcs : e;
+}
+
+__global__ void kp_pieces_count(const unsigned long long *segn_p, const uint32_t *seg_u, const uint64_t *seg_k,
+                                const uint64_t *rs, const uint32_t *adj, unsigned long long *rcnt) {
+    const int64_t segn = (int64_t)*segn_p;
+    PSTRIDE(g, segn) {
+        uint32_t ul;
+        uint64_t k0, k1;
+        seg_bounds(seg_u, seg_k, rs, g, ul, k0, k1);
+        const uint32_t rf = adj[k0] >> kRangeBits, rl = adj[k1 - 1] >> kRangeBits;
+        for (uint32_t r = rf; r <= rl; ++r) atomicAdd(&rcnt[r], 1ull);
+    }
+}
+
+// rcnt[0..R) -> exclusive offsets in rcur[0..R), total in rcur[R]
+__global__ void kp_pieces_scan(int R, const unsigned long long *rcnt, unsigned long long *rcur) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int r = 0; r < R; ++r) {
+            rcur[r] = run;
+            run += rcnt[r];
+        }
+        rcur[R] = run;
+    }
+}
+
+struct Piece {
+    uint64_t a0, a1;  // arc range of the piece
+    uint32_t u, pad;  // local row
+};
+
+// warp per segment, lane per range: the piece bounds are found here (many
+// independent binary searches in flight) rather than by the expanding CTA
+__global__ void kp_pieces_fill(const unsigned long long *segn_p, const uint32_t *seg_u, const uint64_t *seg_k,
+                               const uint64_t *rs, const uint32_t *adj, unsigned long long *rcur,
+                               Piece *pieces) {
+    const int64_t segn = (int64_t)*segn_p;
+    const int lane = threadIdx.x & 31;
+    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < segn;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        uint32_t ul;
+        uint64_t k0, k1;
+        seg_bounds(seg_u, seg_k, rs, g, ul, k0, k1);
+        const uint32_t rf = adj[k0] >> kRangeBits, rl = adj[k1 - 1] >> kRangeBits;
+        for (uint32_t r = rf + lane; r <= rl; r += 32) {
+            uint64_t b[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {  // lower_bound of the range edges in the sorted segment
+                const uint64_t x = (uint64_t)(r + t) << kRangeBits;
+                uint64_t a = k0, c = k1;
+                while (a < c) {
+                    const uint64_t mid = (a + c) >> 1;
+                    if ((uint64_t)adj[mid] < x) a = mid + 1; else c = mid;
+                }
+                b[t] = a;
+            }
+            pieces[atomicAdd(&rcur[r], 1ull)] = Piece{b[0], b[1], ul, 0u};
+        }
+    }
+}
+
 // Top-down expansion.  Every arc into an unvisited target lowers cand[v]
 // (atomicMin) and marks v in the touch bitmap (a reduction, no return): both
 // fire-and-forget.  The records are built afterwards by a scan of the touch
@@ -251,7 +327,8 @@ __device__ __forceinline__ void td_arc(uint32_t v, int32_t u, const uint32_t *V,
 // segment.  Counts are read on the device (no host round trip per layer).
 __global__ void kp_td(const uint32_t *q, const unsigned long long *qn_p, int64_t lo, const uint64_t *rs,
                       const uint32_t *adj, const uint32_t *V, int32_t *cand, uint32_t *touch,
-                      const uint32_t *seg_u, const uint64_t *seg_k, const unsigned long long *segn_p) {
+                      const uint32_t *seg_u, const uint64_t *seg_k, const unsigned long long *segn_p,
+                      const Piece *pieces, const unsigned long long *pieces_n_p) {
     const int lane = threadIdx.x & 31;
     const int64_t qn = (int64_t)*qn_p, segn = (int64_t)*segn_p;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < qn;
@@ -262,13 +339,30 @@ __global__ void kp_td(const uint32_t *q, const unsigned long long *qn_p, int64_t
         const int32_t u = (int32_t)(lo + ul);
         for (uint64_t k = s + lane; k < e; k += 32) td_arc(adj[k], u, V, cand, touch);
     }
-    for (int64_t g = blockIdx.x; g < segn; g += gridDim.x) {
-        const uint32_t ul = seg_u[g];
-        const uint64_t k0 = seg_k[g], e = rs[ul + 1];
-        const uint64_t k1 = k0 + kSegArcs < e ? k0 + kSegArcs : e;
-        const int32_t u = (int32_t)(lo + ul);
-        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) td_arc(adj[k], u, V, cand, touch);
+    (void)segn;
+    // long-row pieces in range order, CTA per piece, 4 arcs per thread per step
+    // (loads of all four issued before their tests)
+    const int64_t npieces = (int64_t)pieces_n_p[0];
+    for (int64_t i = blockIdx.x; i < npieces; i += gridDim.x) {
+        const Piece pc = pieces[i];
+        const int32_t u = (int32_t)(lo + pc.u);
+        for (uint64_t kb = pc.a0; kb < pc.a1; kb += 4 * (uint64_t)blockDim.x) {
+            uint32_t v[4];
+            bool ok[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t k = kb + threadIdx.x + (uint64_t)j * blockDim.x;
+                ok[j] = k < pc.a1;
+                v[j] = ok[j] ? adj[k] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (ok[j]) td_arc(v[j], u, V, cand, touch);
+        }
     }
+    (void)segn;
+    (void)seg_u;
+    (void)seg_k;
 }
 
 __global__ void kp_touch_popc(int64_t W, const uint32_t *touch, uint32_t *cnt) {
@@ -361,6 +455,11 @@ static int part_alloc_state(Part *P) {
         const int64_t nseg = P->arcs / kSegArcs + P->nloc / 1024 + 16;
         HB_CHECK(P->seg_u.alloc(nseg * 4));
         HB_CHECK(P->seg_k.alloc(nseg * 8));
+        P->nseg_cap = nseg;
+        P->ranges = (int)std::max<int64_t>(1, (P->n + (int64_t(1) << kRangeBits) - 1) >> kRangeBits);
+        // a segment splits into at most min(ranges, kSegArcs) pieces
+        HB_CHECK(P->pieces.alloc(nseg * std::min<int64_t>(P->ranges, kSegArcs) * sizeof(Piece) + 16));
+        HB_CHECK(P->rcnt.alloc((2 * P->ranges + 2) * 8));
     }
     HB_CHECK(P->cand.alloc(P->n * 4 + 16));
     HB_CHECK(P->touch.alloc(P->W * 4 + 16));
@@ -608,9 +707,18 @@ extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t world, int64_t *send_co
     kp_queue<<<pgrid(P->wloc), 256, 0, st>>>(P->wloc, P->lo, P->F.as<uint32_t>(), P->rs.as<uint64_t>(),
                                              P->q.as<uint32_t>(), qn, P->seg_u.as<uint32_t>(),
                                              P->seg_k.as<uint64_t>(), qn + 1);
+    unsigned long long *rcnt = P->rcnt.as<unsigned long long>(), *rcur = rcnt + P->ranges;
+    HB_CUDA(cudaMemsetAsync(rcnt, 0, P->ranges * 8, st));
+    kp_pieces_count<<<pgrid(P->nseg_cap), 256, 0, st>>>(qn + 1, P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(),
+                                                       P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), rcnt);
+    kp_pieces_scan<<<1, 32, 0, st>>>(P->ranges, rcnt, rcur);
+    kp_pieces_fill<<<pgrid(P->nseg_cap * 32), 256, 0, st>>>(qn + 1, P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(),
+                                                           P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), rcur,
+                                                           P->pieces.as<Piece>());
     kp_td<<<148 * 8, 256, 0, st>>>(P->q.as<uint32_t>(), qn, P->lo, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
                                    P->V.as<uint32_t>(), P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
-                                   P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(), qn + 1);
+                                   P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(), qn + 1,
+                                   P->pieces.as<Piece>(), rcur + P->ranges);
     uint32_t *cnt = P->wcnt.as<uint32_t>();
     kp_touch_popc<<<pgrid(P->W + 1), 256, 0, st>>>(P->W, P->touch.as<uint32_t>(), cnt);
     size_t tb = P->scan_bytes;
