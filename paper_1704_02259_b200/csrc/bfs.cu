@@ -41,20 +41,10 @@ namespace hbfs {
 
 constexpr int kTdItems = 4;
 constexpr int kTdChunk = kBlock * kTdItems;  // arcs per CTA work item
-// uint4 row probes per lane before the warp-cooperative scan (non-scan layers)
+// uint4 row probes per lane before the warp-cooperative scan: 2 normally, 4 in
+// bottom-up layers whose frontier is tiny (most rows are scanned to the end)
 constexpr int kLaneVecs = 2;
-// Tiny-frontier bottom-up layers (large-graph variants): searches per lane,
-// steps, and uint4 vectors per step (rows are mostly scanned to their end)
-#ifndef HBFS_SCAN_K
-#define HBFS_SCAN_K 2
-#endif
-#ifndef HBFS_SCAN_LV
-#define HBFS_SCAN_LV 4
-#endif
-#ifndef HBFS_SCAN_NV
-#define HBFS_SCAN_NV 1
-#endif
-constexpr int kScanK = HBFS_SCAN_K, kScanLV = HBFS_SCAN_LV, kScanNV = HBFS_SCAN_NV;
+constexpr int kLaneVecsScan = 4;
 constexpr int kTdMaxSub = 8;  // top-down chunk split on small layers (2048 / 8 = 256 arcs per CTA)
 constexpr uint64_t kTailLong = 256;  // open rows longer than this use the whole-warp scan
 // Single first probe when the frontier holds >= n/16 vertices — on graphs
@@ -349,7 +339,7 @@ __device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
 // FIRST1 (dense frontiers, where nearly every found vertex hits at its first
 // entry): probe that entry alone before the vectors — one bitmap load instead
 // of up to four.
-template <typename OffT, int K, int LV, bool FIRST1, int NV = 1>
+template <typename OffT, int K, int LV, bool FIRST1>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                                            const uint32_t *__restrict__ bm_in,
                                            const bool (&act)[K], const OffT (&s)[K],
@@ -383,61 +373,42 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
     }
 #pragma unroll
     for (int it = 0; it < LV; ++it) {
-        // NV aligned uint4 vectors (4*NV entries) per row per step, loads in flight together
-        uint4 q4[K][NV];
+        uint4 q4[K];
         bool go[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             go[k] = act[k] && hit[k] < 0 && p[k] < e[k];
-            const OffT base = p[k] & ~(OffT)3;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                if (go[k] && (v == 0 || base + 4 * v < e[k]))
-                    q4[k][v] = __ldg(reinterpret_cast<const uint4 *>(adj + base + 4 * v));
-                else
-                    q4[k][v] = make_uint4(0, 0, 0, 0);
-            }
+            if (go[k]) q4[k] = __ldg(reinterpret_cast<const uint4 *>(adj + (p[k] & ~(OffT)3)));
+            else q4[k] = make_uint4(0, 0, 0, 0);
         }
-        uint32_t wd[K][NV][4];
+        uint32_t wd[K][4];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const OffT base = p[k] & ~(OffT)3;
+            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const uint32_t val[4] = {q4[k][v].x, q4[k][v].y, q4[k][v].z, q4[k][v].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const OffT idx = base + 4 * v + j;
-                    const bool ok = go[k] && idx >= p[k] && idx < e[k];
-                    wd[k][v][j] = ok ? probe_word(bm, val[j]) : 0u;
-                }
+            for (int j = 0; j < 4; ++j) {
+                const OffT idx = base + j;
+                const bool ok = go[k] && idx >= p[k] && idx < e[k];
+                wd[k][j] = ok ? probe_word(bm, val[j]) : 0u;
             }
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if (!go[k]) continue;
             const OffT base = p[k] & ~(OffT)3;
+            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
             uint32_t hm = 0;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const uint32_t val[4] = {q4[k][v].x, q4[k][v].y, q4[k][v].z, q4[k][v].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) hm |= ((wd[k][v][j] >> (val[j] & 31)) & 1u) << (4 * v + j);
-            }
+            for (int j = 0; j < 4; ++j) hm |= ((wd[k][j] >> (val[j] & 31)) & 1u) << j;
             // wd is 0 for out-of-row entries, so a set bit is always in range
             if (hm) {
                 const int j = __ffs(hm) - 1;
                 hit[k] = (int64_t)(base + j);
-                // select, not an indexed read: a dynamic index would put q4 in local memory
-                uint32_t a = 0;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int jj = j - 4 * v;
-                    a = jj == 0 ? q4[k][v].x : jj == 1 ? q4[k][v].y : jj == 2 ? q4[k][v].z : jj == 3 ? q4[k][v].w : a;
-                }
-                hu[k] = a;
+                // select, not val[j]: a dynamic index would put val[] in local memory
+                hu[k] = j == 0 ? val[0] : j == 1 ? val[1] : j == 2 ? val[2] : val[3];
             } else {
-                p[k] = base + 4 * NV;
+                p[k] = base + 4;
             }
         }
     }
@@ -881,7 +852,7 @@ struct TileSched {
     }
 };
 
-template <typename OffT, int C, int LV, bool FIRST1, int NV = 1>
+template <typename OffT, int C, int LV, bool FIRST1>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
@@ -943,7 +914,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
             int64_t hit[C];
             uint32_t hu[C];
-            first_hits<OffT, C, LV, FIRST1, NV>(A.adj, in.p, act, s, e, hit, hu);
+            first_hits<OffT, C, LV, FIRST1>(A.adj, in.p, act, s, e, hit, hu);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 if (!act[k]) continue;
@@ -1309,7 +1280,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
             if (SCAN && S.v_f * 64 < A.n)
-                phase_bu<OffT, kScanK, kScanLV, false, kScanNV>(A, S, in, out, spare, ctr, red, sf);
+                phase_bu<OffT, K, kLaneVecsScan, false>(A, S, in, out, spare, ctr, red, sf);
             else if (S.v_f * A.first1_div >= A.n)
                 phase_bu<OffT, K, kLaneVecs, true>(A, S, in, out, spare, ctr, red, sf);
             else phase_bu<OffT, K, kLaneVecs, false>(A, S, in, out, spare, ctr, red, sf);
