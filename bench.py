@@ -51,6 +51,11 @@ CONFIGS = {
     "c4": dict(scale=26, probs=(0.57, 0.19, 0.19, 0.05),
                heur=dict(heuristic="beamer", alpha=14, beta=24, counter_mode="edge"),
                ref=dict(alpha=14, beta=24), label="kron_s26_ef16"),
+    # BASELINE config 5's graph (quoted there for 4/8 GPUs) on ONE B200: 34 GB
+    # of adjacency, 64-bit row offsets, source-range CSR build
+    "c5": dict(scale=28, probs=(0.57, 0.19, 0.19, 0.05),
+               heur=dict(heuristic="beamer", alpha=14, beta=24, counter_mode="edge"),
+               ref=dict(alpha=14, beta=24), label="kron_s28_ef16"),
 }
 DEFAULT_CONFIG = "c4"
 ROOTS = 64

@@ -236,11 +236,201 @@ static int alloc_adj(hbfs_graph *g) {
     return HBFS_OK;
 }
 
+// ---- source-range build for graphs whose monolithic key sort does not fit
+// (SCALE 28: 2^33 arcs = 2 x 69 GB of keys).  The vertex range is cut into P
+// pieces; piece r sorts only the arcs whose source lies in it, with keys
+// (src - lo) << sb | dst, and writes its rows at the running arc offset.  Rows
+// come out in (src, dst) order exactly as in the monolithic build (and
+// csr.py:54-64).
+
+// arcs per source piece (both directions of every edge)
+__global__ void k_piece_counts(int64_t m, const uint32_t *u, const uint32_t *v, int64_t span, int P,
+                               unsigned long long *cnt) {
+    extern __shared__ unsigned long long s_cnt[];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        atomicAdd(&s_cnt[u[e] / span], 1ull);
+        atomicAdd(&s_cnt[v[e] / span], 1ull);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        if (s_cnt[i]) atomicAdd(&cnt[i], s_cnt[i]);
+}
+
+// keys of the arcs whose source is in [lo, lo + span); warp-aggregated slots
+__global__ void k_piece_keys(int64_t m, const uint32_t *u, const uint32_t *v, int64_t lo, int64_t span,
+                             int sb, uint64_t *key, unsigned long long *pos) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t m32 = (m + 31) & ~int64_t(31);  // whole warps iterate together
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m32; e += stride) {
+        const bool in = e < m;
+        const uint32_t a = in ? u[e] : 0u, b = in ? v[e] : 0u;
+        const bool fa = in && (int64_t)a >= lo && (int64_t)a < lo + span;
+        const bool fb = in && (int64_t)b >= lo && (int64_t)b < lo + span;
+        const unsigned ba = __ballot_sync(0xffffffffu, fa), bb = __ballot_sync(0xffffffffu, fb);
+        const unsigned tot = __popc(ba) + __popc(bb);
+        if (!tot) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(pos, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned below = (1u << lane) - 1u;
+        if (fa) key[base + __popc(ba & below)] = ((uint64_t)(a - lo) << sb) | b;
+        if (fb) key[base + __popc(ba) + __popc(bb & below)] = ((uint64_t)(b - lo) << sb) | a;
+    }
+}
+
+// rs[lo + i] = off + lower_bound(keys, i << sb) for local rows i in [0, cnt)
+template <typename OffT>
+__global__ void k_piece_row_starts(int64_t lo, int64_t cnt_rows, int64_t arcs, int sb, const uint64_t *key,
+                                   uint64_t off, OffT *rs) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt_rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t target = (uint64_t)i << sb;
+        int64_t a = 0, b = arcs;
+        while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            if (key[mid] < target) a = mid + 1; else b = mid;
+        }
+        rs[lo + i] = (OffT)(off + (uint64_t)a);
+    }
+}
+
+// dedup flags of a piece: keys hold (src - lo) << sb | dst
+__global__ void k_piece_dedup_flags(int64_t arcs, int sb, int64_t lo, const uint64_t *key, uint8_t *keep) {
+    const uint64_t mask = (uint64_t(1) << sb) - 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < arcs;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = key[i];
+        const bool self = (k >> sb) + (uint64_t)lo == (k & mask);
+        const bool dup = i > 0 && key[i - 1] == k;
+        keep[i] = !(self || dup);
+    }
+}
+
+__global__ void k_key_to_adj_off(int64_t arcs, int sb, const uint64_t *key, uint32_t *adj) {
+    const uint64_t mask = (uint64_t(1) << sb) - 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < arcs;
+         i += (int64_t)gridDim.x * blockDim.x)
+        adj[i] = (uint32_t)(key[i] & mask);
+}
+
+template <typename OffT>
+static int build_pieces(const uint32_t *du, const uint32_t *dv, int64_t m, int64_t n, int dedup, int P,
+                        cudaStream_t st, hbfs_graph *g) {
+    const int sb = bits_for(n);
+    const int64_t span = (n + P - 1) / P;
+    const int sl = bits_for(span);
+    if (sl + sb > 64) return set_error(HBFS_ECAPACITY, "vertex ids too wide");
+    DevBuf cnt;
+    HB_CHECK(cnt.alloc(P * 8 + 16));
+    HB_CUDA(cudaMemsetAsync(cnt.p, 0, P * 8, st));
+    k_piece_counts<<<grid_for(m), 256, P * 8, st>>>(m, du, dv, span, P, cnt.as<unsigned long long>());
+    HB_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> hc(P);
+    HB_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, P * 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long mx = 0, tot = 0;
+    for (int r = 0; r < P; ++r) {
+        mx = std::max(mx, hc[r]);
+        tot += hc[r];
+    }
+    // keep-dup arcs bound the output; dedup only shrinks it
+    g->n = n;
+    g->m_edges = m;
+    g->arcs = (int64_t)tot;
+    g->wide = sizeof(OffT) == 8;
+    HB_CHECK(alloc_adj(g));
+    HB_CHECK(g->rs.alloc((n + 1) * sizeof(OffT)));
+    DevBuf k0, k1, tmp, pos, flags, nsel, tmp2;
+    HB_CHECK(k0.alloc(mx * 8 + 8));
+    HB_CHECK(k1.alloc(mx * 8 + 8));
+    HB_CHECK(pos.alloc(16));
+    size_t tb = 0;
+    {
+        cub::DoubleBuffer<uint64_t> db(k0.as<uint64_t>(), k1.as<uint64_t>());
+        HB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)mx, 0, sl + sb, st));
+    }
+    HB_CHECK(tmp.alloc(tb + 16));
+    size_t tb2 = 0;
+    if (dedup) {
+        HB_CHECK(flags.alloc(mx + 16));
+        HB_CHECK(nsel.alloc(16));
+        HB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, k0.as<uint64_t>(), flags.as<uint8_t>(),
+                                           k1.as<uint64_t>(), nsel.as<int64_t>(), (int64_t)mx, st));
+        HB_CHECK(tmp2.alloc(tb2 + 16));
+    }
+    uint64_t off = 0;
+    for (int r = 0; r < P; ++r) {
+        const int64_t lo = r * span, rows = std::max<int64_t>(0, std::min<int64_t>(span, n - lo));
+        if (rows == 0) continue;
+        int64_t c = (int64_t)hc[r];
+        HB_CUDA(cudaMemsetAsync(pos.p, 0, 8, st));
+        k_piece_keys<<<grid_for(m), 256, 0, st>>>(m, du, dv, lo, span, sb, k0.as<uint64_t>(),
+                                                  pos.as<unsigned long long>());
+        HB_CUDA(cudaGetLastError());
+        cub::DoubleBuffer<uint64_t> db(k0.as<uint64_t>(), k1.as<uint64_t>());
+        size_t t = tb;
+        if (c > 0) HB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, t, db, c, 0, sl + sb, st));
+        uint64_t *sorted = db.Current();
+        if (dedup && c > 0) {
+            uint64_t *other = db.Alternate();
+            k_piece_dedup_flags<<<grid_for(c), 256, 0, st>>>(c, sb, lo, sorted, flags.as<uint8_t>());
+            HB_CUDA(cudaGetLastError());
+            size_t t2 = tb2;
+            HB_CUDA(cub::DeviceSelect::Flagged(tmp2.p, t2, sorted, flags.as<uint8_t>(), other,
+                                               nsel.as<int64_t>(), c, st));
+            int64_t h = 0;
+            HB_CUDA(cudaMemcpyAsync(&h, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+            c = h;
+            sorted = other;
+        }
+        if (c > 0) {
+            k_key_to_adj_off<<<grid_for(c), 256, 0, st>>>(c, sb, sorted, g->adj.as<uint32_t>() + off);
+            HB_CUDA(cudaGetLastError());
+        }
+        k_piece_row_starts<OffT><<<grid_for(rows), 256, 0, st>>>(lo, rows, c, sb, sorted, off, g->rs.as<OffT>());
+        HB_CUDA(cudaGetLastError());
+        off += (uint64_t)c;
+        HB_CUDA(cudaStreamSynchronize(st));  // k0/k1 are reused by the next piece
+    }
+    g->arcs = (int64_t)off;
+    if (g->wide) {
+        const uint64_t e = off;
+        HB_CUDA(cudaMemcpyAsync(g->rs.as<uint64_t>() + n, &e, 8, cudaMemcpyHostToDevice, st));
+    } else {
+        const uint32_t e = (uint32_t)off;
+        HB_CUDA(cudaMemcpyAsync(g->rs.as<uint32_t>() + n, &e, 4, cudaMemcpyHostToDevice, st));
+    }
+    HB_CUDA(cudaStreamSynchronize(st));
+    return graph_finalize(g, st);
+}
+
 static int build_from_edges_dev(const uint32_t *du, const uint32_t *dv, int64_t m, int64_t n,
                                 int dedup, cudaStream_t st, hbfs_graph *g) {
     const int sb = bits_for(n);
     if (2 * sb > 64) return set_error(HBFS_ECAPACITY, "vertex ids too wide");
     int64_t arcs = 2 * m;
+    {
+        // monolithic sort: 2 key buffers + adjacency + sort scratch; otherwise
+        // the source-range build with as many pieces as the free memory needs
+        size_t fr = 0, total = 0;
+        cudaMemGetInfo(&fr, &total);
+        const int64_t force = getenv("HBFS_BUILD_PIECES") ? atoll(getenv("HBFS_BUILD_PIECES")) : 0;
+        const double need = (double)arcs * (8 + 8 + 4 + 1) + (double)(n + 1) * 8;
+        if (m > 0 && (force > 1 || need > 0.85 * (double)fr)) {
+            int P = force > 1 ? (int)force : 2;
+            while (force <= 1 && P < 1024 &&
+                   (double)arcs * 4 + (double)arcs / P * (8 + 8 + 1) * 1.3 + (double)(n + 1) * 8 > 0.85 * (double)fr)
+                P *= 2;
+            const bool wide = arcs >= (int64_t(1) << 32) - 1024;
+            return wide ? build_pieces<uint64_t>(du, dv, m, n, dedup, P, st, g)
+                        : build_pieces<uint32_t>(du, dv, m, n, dedup, P, st, g);
+        }
+    }
     DevBuf k0, k1, tmp;
     HB_CHECK(k0.alloc(arcs * 8 + 8));
     HB_CHECK(k1.alloc(arcs * 8 + 8));

@@ -210,3 +210,21 @@ def test_c3_uniform_s22_roots(cuda, golden_hashes):
         assert sha(out.level) == r["level_sha"]
         assert sha(out.parent) == r["simd_default"]["parent_sha"]
         assert trace_array(out.trace).tolist() == r["simd_default"]["trace"]
+
+
+@pytest.mark.parametrize("pieces", [2, 3, 8])
+def test_source_range_build_matches_reference(cuda, golden_hashes, monkeypatch, pieces):
+    """The piecewise CSR build (used when the monolithic key sort does not fit,
+    e.g. SCALE 28 on one GPU), forced on C1: keep-dup and dedup CSR bit-exact."""
+    hb = cuda
+    monkeypatch.setenv("HBFS_BUILD_PIECES", str(pieces))
+    rec = golden_hashes["configs"]["C1_kron_s16"]
+    params = hb.GraphParams(scale=16, edgefactor=16, seed=1)
+    g = hb.generate_graph(params)
+    assert sha(g.row_starts) == rec["rs_sha"] and sha(g.adjacency) == rec["adj_sha"]
+    gd = hb.generate_graph(params, dedup=True)
+    assert gd.num_arcs == rec["dedup_arcs"] and sha(gd.adjacency) == rec["dedup_adj_sha"]
+    assert sha(gd.row_starts) == rec["dedup_rs_sha"]
+    s = int(rec["sources"][0])
+    out = hb.bfs(g, s, hb.HeuristicParams(), use_simd=True, device=False)
+    assert sha(out.level) == rec["roots"][str(s)]["level_sha"]
