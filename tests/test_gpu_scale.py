@@ -80,3 +80,35 @@ def test_c4_kron_s26_vs_reference_kernels(cuda, oracle):
         assert np.array_equal(out.parent, oracle.minid_parents(host, ref_lev, s))
         fp, fl = native.bfs_reference(rs, adj, n, s)
         assert np.array_equal(fl, ref_lev) and np.array_equal(fp, ref_par)
+
+
+def test_s28_kron_one_gpu_vs_reference_kernel(cuda, oracle):
+    """SCALE 28 (BASELINE config 5's graph, 2^33 arcs, 64-bit row offsets,
+    source-range CSR build) on one GPU: levels of one root against the
+    reference's compiled bfs_reference, parents against the min-id rule."""
+    import torch
+
+    hb = cuda
+    from oracle import refnative
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < (150 << 30):
+        pytest.skip("needs a 180 GB B200")
+    with open("/proc/meminfo") as fh:
+        mem_kb = int(next(x for x in fh if x.startswith("MemAvailable")).split()[1])
+    if mem_kb < (100 << 20):
+        pytest.skip("needs ~80 GB of host memory for the reference run")
+    nat = refnative.load()
+    assert nat is not None
+    g = hb.generate_graph(hb.GraphParams(scale=28, edgefactor=16, seed=1))
+    assert g.wide_offsets and g.num_arcs == 1 << 33
+    s = int(hb.sample_sources(g, 1, 1)[0])
+    out = hb.bfs(g, s, hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge"),
+                 device=False)
+    n = g.num_vertices
+    rs, adj = g.row_starts, g.adjacency
+    g.free()
+    _, ref_lev = nat.bfs_reference(rs, adj, n, s)
+    assert np.array_equal(out.level, ref_lev)
+    host = oracle.HostCsr(n, rs, adj, 1 << 32)
+    assert np.array_equal(out.parent, oracle.minid_parents(host, ref_lev, s))
