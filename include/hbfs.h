@@ -205,6 +205,9 @@ int hbfs_part_init(hbfs_part *p, int64_t root, void *stream);
  * degree sum, gathers, fallbacks} (the reference's 16-lane counters). */
 int hbfs_part_bu(hbfs_part *p, int32_t depth, int32_t max_pos, uint32_t *next_slice,
                  unsigned long long *counters, void *stream);
+/* Optional: global frontier size of the coming bottom-up layer (picks the
+ * tiny-frontier probe variant as the single-GPU kernel does). */
+int hbfs_part_hint_frontier(hbfs_part *p, int64_t v_f);
 /* Top-down expansion of the owned frontier for a `world`-rank partition:
  * every unvisited target is queued once for its owner with this rank's min
  * parent candidate; send_counts: device int64[world] = records per owner. */

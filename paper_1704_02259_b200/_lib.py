@@ -81,6 +81,7 @@ SIGNATURES = {
     "hbfs_part_free": (C.c_int, [P]),
     "hbfs_part_init": (C.c_int, [P, i64, P]),
     "hbfs_part_bu": (C.c_int, [P, i32, i32, P, P, P]),
+    "hbfs_part_hint_frontier": (C.c_int, [P, i64]),
     "hbfs_part_td_expand": (C.c_int, [P, i32, P, P]),
     "hbfs_part_td_pack": (C.c_int, [P, P, P]),
     "hbfs_part_td_apply": (C.c_int, [P, i32, P, i64, P, P, P]),

@@ -120,6 +120,7 @@ struct Args {
     int max_pos, use_simd, parent_mode, do_init;
     int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
     int64_t first1_div;  // bottom-up probes a row's first entry alone when v_f >= n / first1_div
+    int64_t part_w0, part_wend;  // partition bottom-up (PART): owned word range
     uint32_t root;
 };
 
@@ -852,7 +853,10 @@ struct TileSched {
     }
 };
 
-template <typename OffT, int C, int LV, bool FIRST1>
+// PART: one rank's share of a 1D partition (csrc/part.cu): tiles cover the
+// owned words [part_w0, part_wend) only; the arrays indexed by vertex or word
+// are offset pointers (see part_bu_launch), and there is no depth ring.
+template <typename OffT, int C, int LV, bool FIRST1, bool PART = false>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
@@ -863,16 +867,18 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t max_pos = A.max_pos;
     // packed per-thread counters: found<<35 | their degree sum ; fallbacks<<35 | gathers
     unsigned long long c_fd = 0, c_fg = 0;
-    const int64_t ntiles = (A.nw + 31) >> 5;
+    const int64_t w0 = PART ? A.part_w0 : 0, wend = PART ? A.part_wend : A.nw;
+    const int64_t ntiles = (wend - w0 + 31) >> 5;
 
     TileSched ts(&A.ctl->work[S.layer % 3], tid >> 5, nth >> 5);
     for (int64_t tile = ts.tile; tile < ntiles; tile = ts.next()) {
-        const int64_t wl = tile * 32 + lane;
-        const bool valid = wl < A.nw;
+        const int64_t tw = w0 + tile * 32;  // first word of the tile
+        const int64_t wl = tw + lane;
+        const bool valid = wl < wend;
         const uint32_t vis0 = valid ? vis[wl] : ~0u;
         const uint32_t inl = valid ? in[wl] : 0u;
         const uint32_t pwl = valid ? __ldg(A.posw + wl) : 0u;
-        if (valid) clear_spare_word(A, S.layer, wl);
+        if (!PART && valid) clear_spare_word(A, S.layer, wl);
         const uint32_t vwl = vis0 | inl;
         const uint32_t candl = ~vwl & pwl;
         if (valid && vwl != vis0) vis[wl] = vwl;  // commit a lagging frontier
@@ -905,7 +911,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 const uint32_t cm = __shfl_sync(full, candl, j);
                 const uint32_t ex = __shfl_sync(full, incl, j) - __shfl_sync(full, cntl, j);
                 const uint32_t bit = act[k] ? nth_bit(cm, c - ex) : 0u;
-                v[k] = (uint32_t)((tile * 32 + j) * 32 + bit);
+                v[k] = (uint32_t)((tw + j) * 32 + bit);
                 s[k] = e[k] = 0;
                 if (act[k]) {
                     s[k] = __ldg(A.rs + v[k]);
@@ -925,7 +931,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 if (found) {
                     A.parent[v[k]] = hu[k];
                     if (A.direct_levels) A.level[v[k]] = (int32_t)S.layer + 1;
-                    atomicOr(&s_found[(v[k] >> 5) - tile * 32], 1u << (v[k] & 31));
+                    atomicOr(&s_found[(v[k] >> 5) - tw], 1u << (v[k] & 31));
                     c_fd += (1ull << kPackShift) + (unsigned long long)deg;
                 }
                 c_fg += (unsigned long long)(early ? pos + 1 : (deg < max_pos ? deg : max_pos));
@@ -1339,6 +1345,75 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         c->rows = rows;
         c->done = S.v_f == 0;
     }
+}
+
+// ------------------------------------------------- partition bottom-up
+
+// One rank's bottom-up layer with the persistent kernel's tile machinery
+// (phase_bu<PART>): called by hbfs_part_bu (csrc/part.cu) as a plain launch.
+template <typename OffT, int K, int LV>
+__global__ void __launch_bounds__(kBlock, 2) part_bu_kernel(Args<OffT> A, St S, Ctr *ctr, const uint32_t *inp,
+                                                          uint32_t *outp) {
+    __shared__ unsigned long long red[(kBlock / 32) * 4];
+    __shared__ uint32_t s_found[kBlock];
+    phase_bu<OffT, K, LV, false, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
+                                       ctr, red, s_found + (threadIdx.x & ~31));
+}
+
+// Ctr (found << 35 | degree sum, gathers, fallbacks) -> {found, degree sum, gathers, fallbacks}
+__global__ void part_bu_counters(const Ctr *c, unsigned long long *out) {
+    out[0] = c->packed >> kPackShift;
+    out[1] = c->packed & kPackMask;
+    out[2] = c->gathers;
+    out[3] = c->fallbacks;
+}
+
+size_t part_bu_scratch_bytes() { return sizeof(Ctl) + 64; }
+
+int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local, int64_t n,
+                   int64_t lo, int64_t nloc, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
+                   int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
+                   unsigned long long *counters, void *scratch, cudaStream_t st) {
+    const int64_t wlo = lo >> 5, wown = (nloc + 31) / 32;
+    Args<uint64_t> A;
+    memset(&A, 0, sizeof(A));
+    // vertex- and word-indexed arrays are offset so that global ids index them
+    A.rs = rs_local - lo;
+    A.adj = adj;
+    A.posw = posw_local - wlo;
+    A.n = n;
+    A.nw = (n + 31) / 32;
+    A.parent = parent_local - lo;
+    A.level = level_local - lo;
+    A.bits = V;
+    A.direct_levels = 1;
+    A.max_pos = max_pos;
+    A.ctl = static_cast<Ctl *>(scratch);
+    A.part_w0 = wlo;
+    A.part_wend = wlo + wown;
+    St S;
+    memset(&S, 0, sizeof(S));
+    S.layer = depth;
+    S.v_f = v_f;
+    Ctr *ctr = &A.ctl->ctr[0];
+    HB_CUDA(cudaMemsetAsync(scratch, 0, sizeof(Ctl), st));
+    static int grid = 0;
+    if (!grid) {
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, part_bu_kernel<uint64_t, 2, kLaneVecs>,
+                                                              kBlock, 0));
+        grid = std::max(1, per_sm) * sms;
+    }
+    uint32_t *outp = next_slice - wlo;
+    if (v_f >= 0 && v_f * 64 < n)  // tiny frontier: rows are mostly scanned to their end
+        part_bu_kernel<uint64_t, 2, kLaneVecsScan><<<grid, kBlock, 0, st>>>(A, S, ctr, F, outp);
+    else
+        part_bu_kernel<uint64_t, 2, kLaneVecs><<<grid, kBlock, 0, st>>>(A, S, ctr, F, outp);
+    part_bu_counters<<<1, 1, 0, st>>>(ctr, counters);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
 }
 
 // ------------------------------------------------------------ variants

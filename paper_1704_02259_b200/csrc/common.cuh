@@ -99,6 +99,15 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
     return cur;
 }
 
+// Bottom-up layer of one partition rank with the persistent kernel's tile
+// machinery (defined in bfs.cu, used by part.cu).  v_f: global frontier size
+// (< 0: unknown).  scratch: part_bu_scratch_bytes() of device memory.
+size_t part_bu_scratch_bytes();
+int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local, int64_t n,
+                   int64_t lo, int64_t nloc, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
+                   int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
+                   unsigned long long *counters, void *scratch, cudaStream_t st);
+
 }  // namespace hbfs
 
 struct hbfs_graph {

@@ -5,6 +5,8 @@
 // replicated (n bits each); parent/level are owned-only.  Per layer the host
 // (paper_1704_02259_b200/mgpu.py) runs one of
 //   bottom-up:  hbfs_part_bu        -> next-frontier slice of the owned words
+//                                      (the persistent kernel's tile code,
+//                                      bfs.cu part_bu_launch)
 //   top-down:   hbfs_part_td_expand -> min parent candidate per unvisited
 //                                      target + a touch bitmap (fire-and-
 //                                      forget reductions), scanned into
@@ -41,6 +43,9 @@ struct Part {
     int64_t nseg_cap = 0;
     int ranges = 1;
     DevBuf scratch;           // counters etc.
+    DevBuf posw;              // uint32[wloc] deg > 0 bits of the owned vertices
+    DevBuf bu_scratch;        // part_bu_launch scratch (Ctl)
+    int64_t fhint = -1;       // global frontier size of the next bottom-up layer (-1: unknown)
     // top-down exchange state (all kept clean between layers)
     DevBuf cand;              // int32[n]  min parent candidate per target (INT32_MAX = none)
     DevBuf touch;             // uint32[W] target already queued this layer
@@ -120,92 +125,6 @@ __global__ void kp_init(int64_t nloc, int64_t W, int64_t lo, uint32_t root, uint
         const uint32_t b = (w == (int64_t)(root >> 5)) ? (1u << (root & 31)) : 0u;
         F[w] = b;
         V[w] = b;
-    }
-}
-
-// Bottom-up over the owned words: warp per word, lane per vertex, row probes in
-// ascending position with warp-cooperative tails (first hit = min position).
-__global__ void kp_bu(int64_t wloc, int64_t nloc, int64_t lo, int32_t depth1, int64_t max_pos,
-                      const uint64_t *rs, const uint32_t *adj, const uint32_t *F, uint32_t *V,
-                      uint32_t *parent, int32_t *level, uint32_t *next,
-                      unsigned long long *ctr) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wlo = lo >> 5;
-    unsigned long long c_cnt = 0, c_deg = 0, c_gat = 0, c_fb = 0;
-    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < wloc;
-         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t vw = V[wlo + j];
-        const int64_t lv = j * 32 + lane;  // local vertex
-        const bool valid = lv < nloc;
-        const uint64_t s = valid ? rs[lv] : 0, e = valid ? rs[lv + 1] : 0;
-        const bool mine = valid && !((vw >> lane) & 1u) && e > s;
-        int64_t hit = -1;
-        uint32_t hu = 0;
-        uint64_t p = s;
-        if (mine) {
-            for (int it = 0; it < 8 && p < e; ++it, ++p) {
-                const uint32_t a = adj[p];
-                if ((F[a >> 5] >> (a & 31)) & 1u) {
-                    hit = (int64_t)p;
-                    hu = a;
-                    break;
-                }
-            }
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, mine && hit < 0 && p < e);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint64_t ps = __shfl_sync(0xffffffffu, p, src), pe = __shfl_sync(0xffffffffu, e, src);
-            int64_t h = -1;
-            uint32_t hv = 0;
-            for (uint64_t c = ps; c < pe; c += 32) {
-                const uint64_t k = c + lane;
-                uint32_t a = 0;
-                const bool bit = k < pe && ((F[(a = adj[k]) >> 5] >> (a & 31)) & 1u);
-                const unsigned b = __ballot_sync(0xffffffffu, bit);
-                if (b) {
-                    const int l = __ffs(b) - 1;
-                    h = (int64_t)(c + l);
-                    hv = __shfl_sync(0xffffffffu, a, l);
-                    break;
-                }
-            }
-            if (lane == src) {
-                hit = h;
-                hu = hv;
-            }
-        }
-        const bool found = hit >= 0;
-        if (found) {
-            parent[lv] = hu;
-            level[lv] = depth1;
-        }
-        const unsigned fm = __ballot_sync(0xffffffffu, found);
-        if (lane == 0) next[j] = fm;
-        if (mine) {
-            const int64_t deg = (int64_t)(e - s);
-            const int64_t pos = found ? hit - (int64_t)s : -1;
-            const bool early = found && pos < max_pos;
-            if (found) {
-                c_cnt += 1;
-                c_deg += (unsigned long long)deg;
-            }
-            c_gat += early ? (unsigned long long)(pos + 1) : (unsigned long long)(deg < max_pos ? deg : max_pos);
-            c_fb += (deg > max_pos && !early) ? 1ull : 0ull;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        c_cnt += __shfl_down_sync(0xffffffffu, c_cnt, o);
-        c_deg += __shfl_down_sync(0xffffffffu, c_deg, o);
-        c_gat += __shfl_down_sync(0xffffffffu, c_gat, o);
-        c_fb += __shfl_down_sync(0xffffffffu, c_fb, o);
-    }
-    if (lane == 0) {
-        if (c_cnt) atomicAdd(&ctr[0], c_cnt);
-        if (c_deg) atomicAdd(&ctr[1], c_deg);
-        if (c_gat) atomicAdd(&ctr[2], c_gat);
-        if (c_fb) atomicAdd(&ctr[3], c_fb);
     }
 }
 
@@ -444,6 +363,17 @@ __global__ void kp_absorb(int64_t W, const uint32_t *next, uint32_t *F, uint32_t
     }
 }
 
+__global__ void kp_posw(int64_t nloc, int64_t wloc, const uint64_t *rs, uint32_t *posw) {
+    PSTRIDE(w, wloc) {
+        uint32_t b = 0;
+        for (int j = 0; j < 32; ++j) {
+            const int64_t v = w * 32 + j;
+            if (v < nloc && rs[v + 1] > rs[v]) b |= 1u << j;
+        }
+        posw[w] = b;
+    }
+}
+
 static int part_alloc_state(Part *P) {
     HB_CHECK(P->F.alloc(P->W * 4 + 16));
     HB_CHECK(P->V.alloc(P->W * 4 + 16));
@@ -451,6 +381,10 @@ static int part_alloc_state(Part *P) {
     HB_CHECK(P->level.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->q.alloc(P->nloc * 4 + 16));
     HB_CHECK(P->scratch.alloc(64));
+    HB_CHECK(P->posw.alloc(P->wloc * 4 + 16));
+    HB_CHECK(P->bu_scratch.alloc(part_bu_scratch_bytes()));
+    HB_CUDA(cudaDeviceSynchronize());  // rs was built on the caller's stream
+    kp_posw<<<pgrid(P->wloc), 256>>>(P->nloc, P->wloc, P->rs.as<uint64_t>(), P->posw.as<uint32_t>());
     {
         const int64_t nseg = P->arcs / kSegArcs + P->nloc / 1024 + 16;
         HB_CHECK(P->seg_u.alloc(nseg * 4));
@@ -678,15 +612,21 @@ extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32
     HB_ENTRY_BEGIN
     if (!P || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    HB_CUDA(cudaMemsetAsync(counters, 0, 32, st));
-    kp_bu<<<pgrid(P->wloc * 32), 256, 0, st>>>(P->wloc, P->nloc, P->lo, depth + 1, max_pos,
-                                               P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-                                               P->F.as<uint32_t>(), P->V.as<uint32_t>(),
-                                               P->parent.as<uint32_t>(), P->level.as<int32_t>(),
-                                               next_slice, counters);
-    HB_CUDA(cudaGetLastError());
+    // the persistent kernel's bottom-up tiles on the owned words (bfs.cu)
+    HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->n, P->lo,
+                            P->nloc, P->F.as<uint32_t>(), P->V.as<uint32_t>(), P->parent.as<uint32_t>(),
+                            P->level.as<int32_t>(), next_slice, depth, max_pos, P->fhint, counters,
+                            P->bu_scratch.p, st));
     return HBFS_OK;
     HB_ENTRY_END
+}
+
+// Global frontier size of the coming bottom-up layer (selects the tiny-frontier
+// probe variant, as on one GPU); optional.
+extern "C" int hbfs_part_hint_frontier(hbfs_part *P, int64_t v_f) {
+    if (!P) return set_error(HBFS_EINVAL, "null part");
+    P->fhint = v_f;
+    return HBFS_OK;
 }
 
 // Top-down expansion of the owned frontier for a `world`-rank partition (owner
@@ -977,6 +917,7 @@ extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_pa
         const int d = decide(H, cur, v_f, e_f, eu_v, eu_e, prev_vf, &fv, &gv);
         HB_CUDA(cudaMemsetAsync(slice, 0, wper * 4, st));
         if (d == HBFS_BOTTOM_UP) {
+            P->fhint = v_f;
             HB_CHECK(hbfs_part_bu(P, (int32_t)layer, p->max_pos, slice, ctr, st));
         } else {
             HB_CHECK(hbfs_part_td_expand(P, world, sc, st));

@@ -262,6 +262,9 @@ class CudaRankOps:
     def init(self, root: int):
         self._lib.check(self.lib.hbfs_part_init(self.h, root, self._s()))
 
+    def hint_frontier(self, v_f: int):
+        self._lib.check(self.lib.hbfs_part_hint_frontier(self.h, int(v_f)))
+
     def bu(self, depth, max_pos, next_slice, ctr):
         self._lib.check(self.lib.hbfs_part_bu(self.h, depth, max_pos, C.c_void_p(next_slice.data_ptr()),
                                               C.c_void_p(ctr.data_ptr()), self._s()))
@@ -359,6 +362,8 @@ class DistBfs:
             tl = time.perf_counter()
             if d == 1:
                 for r, s, c in zip(R, slices, ctrs):
+                    if hasattr(r, "hint_frontier"):
+                        r.hint_frontier(v_f)
                     r.bu(layer, cfg.max_pos, s, c)
             else:
                 for r, sc in zip(R, scounts):
