@@ -229,9 +229,10 @@ int hbfs_part_outputs(hbfs_part *p, uint32_t *parent, int32_t *level, int on_dev
  * hbfs_nccl_unique_id on rank 0 (bytes >= 128), broadcast by the caller, then
  * hbfs_mg_init on every rank (current CUDA device).  hbfs_mg_bfs runs the whole
  * per-layer loop of hybrid.py:83-175 for this rank's hbfs_part (built for the
- * same world/rank split as mgpu.partition): NCCL all-gather of the next
- * frontier, all-reduce of the counters, grouped send/recv of the top-down
- * record counts and records.  trace (may be NULL): identical rows on every
+ * same world/rank split as mgpu.partition), one launch of the persistent
+ * traversal kernel per layer on the owned vertices (min-id parents): NCCL
+ * all-gather of the next frontier, all-reduce of the counters, grouped
+ * send/recv of the top-down record counts and records.  trace (may be NULL): identical rows on every
  * rank (elapsed = 0); device_ms: this rank's CUDA-event time. */
 typedef struct hbfs_mg hbfs_mg;
 int hbfs_nccl_unique_id(void *out, int64_t bytes);
@@ -240,6 +241,11 @@ int hbfs_mg_free(hbfs_mg *m);
 int hbfs_mg_bfs(hbfs_mg *m, hbfs_part *p, int64_t root, const hbfs_params *params,
                 hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers, float *device_ms,
                 void *stream);
+/* The same loop for all `world` parts of a partition held by this process on
+ * one device (exchanges are device copies): P ranks tested on one GPU. */
+int hbfs_mgl_bfs(hbfs_part **parts, int32_t world, int64_t root, const hbfs_params *params,
+                 hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers, float *device_ms,
+                 void *stream);
 
 #ifdef __cplusplus
 }

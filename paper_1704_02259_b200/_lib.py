@@ -91,6 +91,7 @@ SIGNATURES = {
     "hbfs_mg_init": (C.c_int, [P, i32, i32, C.POINTER(P)]),
     "hbfs_mg_free": (C.c_int, [P]),
     "hbfs_mg_bfs": (C.c_int, [P, P, i64, C.POINTER(hbfs_params), P, i64, P, P, P]),
+    "hbfs_mgl_bfs": (C.c_int, [P, i32, i64, C.POINTER(hbfs_params), P, i64, P, P, P]),
 }
 
 _lib = None

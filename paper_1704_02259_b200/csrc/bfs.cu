@@ -30,6 +30,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <vector>
 
@@ -120,7 +121,9 @@ struct Args {
     int max_pos, use_simd, parent_mode, do_init;
     int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
     int64_t first1_div;  // bottom-up probes a row's first entry alone when v_f >= n / first1_div
-    int64_t part_w0, part_wend;  // partition bottom-up (PART): owned word range
+    int64_t part_w0, part_wend;  // partition (PART): owned word range
+    int64_t part_lo, part_nown;  // partition (PART): owned vertex range
+    uint32_t *cand, *touch;      // partition top-down: remote targets' min parent / touched bits
     uint32_t root;
 };
 
@@ -206,6 +209,20 @@ __device__ __forceinline__ void clear_spare_word(const A_t &A, int64_t L, int64_
 
 __device__ __forceinline__ bool test_bit(const Plane &bm, uint32_t a) {
     return (bm[a >> 5] >> (a & 31)) & 1u;
+}
+
+// Partition mode: is vertex v owned by this rank?
+template <bool PART, typename A_t>
+__device__ __forceinline__ bool owned_v(const A_t &A, uint32_t v) {
+    return !PART || (uint64_t)((int64_t)v - A.part_lo) < (uint64_t)A.part_nown;
+}
+// Partition mode: a top-down arc into a vertex of another rank: keep the
+// smallest parent per target and mark it for the record exchange (csrc/part.cu)
+template <typename A_t>
+__device__ __forceinline__ void remote_arc(const A_t &A, uint32_t v, uint32_t u) {
+    const uint32_t b = 1u << (v & 31);
+    atomicMin(&A.cand[v], u);
+    if (!(__ldcg(&A.touch[v >> 5]) & b)) atomicOr(&A.touch[v >> 5], b);
 }
 
 // Bitmap probe through a raw pointer with a 32-bit word index: one wide
@@ -515,12 +532,13 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
 
 // ---------------------------------------------------------------- phases
 
-template <typename OffT>
+template <typename OffT, bool PART = false>
 __device__ void phase_init(const Args<OffT> &A) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const uint32_t root = A.root;
-    for (int64_t i = tid; i < A.n; i += nth) {
+    const int64_t v0 = PART ? A.part_lo : 0, v1 = PART ? A.part_lo + A.part_nown : A.n;
+    for (int64_t i = v0 + tid; i < v1; i += nth) {
         const bool r = i == (int64_t)root;
         A.parent[i] = r ? root : HBFS_NIL;
         if (A.direct_levels) A.level[i] = r ? 0 : -1;
@@ -530,14 +548,18 @@ __device__ void phase_init(const Args<OffT> &A) {
     const uint32_t rb = 1u << (root & 31);
     for (int64_t w = tid; w < 3 * A.nw; w += nth)  // vis, depth plane 0 (root), plane 1
         A.bits[w] = (w == rw || w == A.nw + rw) ? rb : 0u;
-    const OffT r0 = __ldg(A.rs + root);
-    const uint64_t rdeg = (uint64_t)(__ldg(A.rs + root + 1) - r0);
-    const uint64_t nch = (rdeg + kTdChunk - 1) / kTdChunk;
-    for (int64_t c = tid; c < (int64_t)nch; c += nth) A.qb[0].cs[c] = 0;
+    if (!PART) {  // partitions convert the root plane instead
+        const OffT r0 = __ldg(A.rs + root);
+        const uint64_t rdeg = (uint64_t)(__ldg(A.rs + root + 1) - r0);
+        const uint64_t nch = (rdeg + kTdChunk - 1) / kTdChunk;
+        for (int64_t c = tid; c < (int64_t)nch; c += nth) A.qb[0].cs[c] = 0;
+        if (tid == 0) {
+            A.qb[0].q[0] = root;
+            A.qb[0].qo[0] = 0;
+            A.qb[0].qr[0] = r0;
+        }
+    }
     if (tid == 0) {
-        A.qb[0].q[0] = root;
-        A.qb[0].qo[0] = 0;
-        A.qb[0].qr[0] = r0;
         Ctl *c = A.ctl;
         for (int s = 0; s < 3; ++s) {
             c->ctr[s] = Ctr{0, 0, 0, 0};
@@ -591,7 +613,7 @@ __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare)
 // SPAN: base chunks (of kTdChunk arcs) per work item; harvest layers use 2.
 // Small layers split a chunk into `nsub` sub-items (part `sub`) so that more
 // CTAs share it: a single SM's request rate, not latency, bounds a lone chunk.
-template <typename OffT, bool Harvest, int SPAN>
+template <typename OffT, bool Harvest, int SPAN, bool PART = false>
 __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
                                          uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
                                          const Plane in, const Plane out, const Queue<OffT> &NQ,
@@ -655,6 +677,10 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
             for (int k = 0; k < I; ++k) {
                 const uint32_t b = 1u << (v[k] & 31);
                 if (!(vw[k] & b)) {
+                    if (!owned_v<PART>(A, v[k])) {
+                        remote_arc(A, v[k], u[k]);
+                        continue;
+                    }
                     atomicOr(&out[v[k] >> 5], b);
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
@@ -687,7 +713,9 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
             for (int k = 0; k < I; ++k) {
                 const uint32_t b = 1u << (v[k] & 31);
                 claim[k] = false;
-                if (!(vw[k] & b)) {
+                if (!(vw[k] & b) && !owned_v<PART>(A, v[k])) {
+                    remote_arc(A, v[k], u[k]);
+                } else if (!(vw[k] & b)) {
                     uint32_t old = ow[k];
                     if (!(old & b)) old = atomicOr(&out[v[k] >> 5], b);
                     claim[k] = !(old & b);
@@ -715,7 +743,7 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
 // atomicOr on an L2-resident bitmap; min-id mode adds atomicMin(parent) for
 // every arc into a vertex unvisited before the layer.  Replaces
 // top_down_layer / top_down_chunked (_native.pyx:65-86, :207-239).
-template <typename OffT, bool Harvest>
+template <typename OffT, bool Harvest, bool PART = false>
 __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
@@ -731,8 +759,8 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
     if (!Harvest)
         while (nsub < kTdMaxSub && nitems * nsub * 4 <= (int64_t)gridDim.x) nsub *= 2;
     for (int64_t g = blockIdx.x; g < nitems * nsub; g = block_grab(work, &sm.item))
-        td_chunk<OffT, Harvest, SPAN>(A, Q, nf, mf, (g / nsub) * SPAN, nchunks, (int32_t)S.layer + 1, in,
-                                      out, NQ, ctr, sm, (int)(g % nsub), nsub);
+        td_chunk<OffT, Harvest, SPAN, PART>(A, Q, nf, mf, (g / nsub) * SPAN, nchunks, (int32_t)S.layer + 1,
+                                            in, out, NQ, ctr, sm, (int)(g % nsub), nsub);
 }
 
 template <typename OffT>
@@ -794,7 +822,7 @@ __device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spa
 // Column-blocked top-down, phase B: all CTAs walk the chunks of range 0, then
 // range 1, ... (one global chunk index space), so the frontier's arcs hit one
 // target range at a time.
-template <typename OffT, bool Harvest>
+template <typename OffT, bool Harvest, bool PART = false>
 __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                              Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre) {
     const int P = A.cb_ranges;
@@ -821,8 +849,8 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
         const uint64_t mf_r = t & kPackMask;
         const Queue<OffT> R = cb_queue(A, r, kCbMaxF);
         const int64_t nch_r = (int64_t)((mf_r + kTdChunk - 1) / kTdChunk);
-        td_chunk<OffT, Harvest, SPAN>(A, R, nf_r, mf_r, (g - s_pre[r]) * SPAN, nch_r, (int32_t)S.layer + 1,
-                 in, out, NQ, ctr, sm);
+        td_chunk<OffT, Harvest, SPAN, PART>(A, R, nf_r, mf_r, (g - s_pre[r]) * SPAN, nch_r,
+                                            (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
     }
 }
 
@@ -1039,18 +1067,19 @@ __device__ __forceinline__ uint64_t word_degsum(const Args<OffT> &A, int64_t w, 
 // words with one reservation; rounds without any frontier bit cost one barrier.
 constexpr int kConvWords = 4;
 
-template <typename OffT>
+template <typename OffT, bool PART = false>
 __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const Plane bm,
                               unsigned long long *counter, bool commit_vis, EnqSmem &es) {
     const Plane vis{A.bits};
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int wpt = A.nw >= kConvWords * nth ? kConvWords : (int)(A.nw / nth > 1 ? A.nw / nth : 1);
+    const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw, nwo = wb - wa;
+    const int wpt = nwo >= kConvWords * nth ? kConvWords : (int)(nwo / nth > 1 ? nwo / nth : 1);
     const int64_t span = (int64_t)blockDim.x * wpt;
-    for (int64_t b0 = (int64_t)blockIdx.x * span; b0 < A.nw; b0 += (int64_t)gridDim.x * span) {
+    for (int64_t b0 = wa + (int64_t)blockIdx.x * span; b0 < wb; b0 += (int64_t)gridDim.x * span) {
         const int64_t w0 = b0 + (int64_t)threadIdx.x * wpt;
         uint32_t bits[kConvWords];
 #pragma unroll
-        for (int i = 0; i < kConvWords; ++i) bits[i] = i < wpt && w0 + i < A.nw ? bm[w0 + i] : 0u;
+        for (int i = 0; i < kConvWords; ++i) bits[i] = i < wpt && w0 + i < wb ? bm[w0 + i] : 0u;
         uint32_t cnt = 0;
         uint64_t dsum = 0;
 #pragma unroll
@@ -1074,14 +1103,15 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
 // were set by reductions (a vertex was discovered iff it was unvisited before
 // the layer and some frontier arc reached it).  Thread per word: vis commit,
 // count and degree sum of the found vertices (and their levels on small graphs).
-template <typename OffT>
+template <typename OffT, bool PART = false>
 __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
                               unsigned long long *red, int32_t depth1) {
     const Plane vis{A.bits};
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
-    for (int64_t w = tid; w < A.nw; w += nth) {
+    const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw;
+    for (int64_t w = wa + tid; w < wb; w += nth) {
         const uint32_t bits = __ldcg(&out[w]);  // set by the expansion's reductions
         if (bits) {
             vis[w] |= bits;
@@ -1193,7 +1223,11 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
 // MINB: CTAs per SM the register allocation must allow.
 // SCAN: also compile the 4-vector bottom-up path for tiny-frontier layers
 // (large graphs only; it costs registers on the small-graph variant).
-template <typename OffT, int K, int MINB, bool SCAN>
+// PART: one layer of one rank's share of a 1D partition per launch (the host
+// loop in csrc/part.cu exchanges records and frontier slices between launches
+// and writes the global controller state into ctl); min-id parents, levels
+// stamped at discovery, the frontier queue always rebuilt from the owned words.
+template <typename OffT, int K, int MINB, bool SCAN, bool PART = false>
 __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -1207,9 +1241,11 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
     unsigned long long *kstamp = A.phase_ns + kRowsCap * kPhaseSlots;  // kernel-level marks
     if (leader) kstamp[0] = globaltimer();
     if (A.do_init) {
-        phase_init(A);
+        phase_init<OffT, PART>(A);
         grid.sync();
         if (leader) kstamp[1] = globaltimer();
+    }
+    if (A.do_init && !PART) {
         const int64_t rdeg = (int64_t)(__ldg(A.rs + A.root + 1) - __ldg(A.rs + A.root));
         S.layer = 0;
         S.v_f = 1;
@@ -1219,7 +1255,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         S.prev_vf = 0;
         S.dir = HBFS_TOP_DOWN;
         S.kind = 0;
-    } else {
+    } else {  // resumed, or (PART) the global state written by the host
         const Ctl *c = A.ctl;
         S.layer = __ldcg(&c->layer);
         S.v_f = __ldcg(&c->v_f);
@@ -1245,51 +1281,64 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         const Plane in = depth_plane(A, L), out = depth_plane(A, L + 1),
                     spare = depth_plane(A, L + 2);
         Ctr *ctr = &A.ctl->ctr[L % 3];
-        if (dir == HBFS_TOP_DOWN && S.kind == 1) {
-            phase_convert(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
+        // SQ: the frontier queue's size (the layer's counts on one GPU; the
+        // rank's own share, from the conversion, in a partition)
+        St SQ = S;
+        if (dir == HBFS_TOP_DOWN && (PART || S.kind == 1)) {
+            phase_convert<OffT, PART>(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
             grid.sync();
             STAMP(1);
+            if (PART) {
+                const unsigned long long cv = __ldcg(&A.ctl->conv);
+                SQ.v_f = (int64_t)(cv >> kPackShift);
+                SQ.e_f = (int64_t)(cv & kPackMask);
+            }
         }
-        const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && S.e_f >= A.cb_min_arcs &&
-                        S.v_f <= kCbMaxF;
+        const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && SQ.e_f >= A.cb_min_arcs &&
+                        SQ.v_f <= kCbMaxF;
         // Slot (L+1)%3 was last read right after the barrier that ended layer
         // L-2, so every CTA is past that read; it must be zero when layer L+1
         // starts accumulating.  The conversion counter is free again too.
         if (leader) {
             A.ctl->ctr[(L + 1) % 3] = Ctr{0, 0, 0, 0};
             A.ctl->work[(L + 1) % 3] = 0;
-            A.ctl->conv = 0;
+            if (!PART) A.ctl->conv = 0;  // PART: the host resets it (other CTAs read it above)
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
-        const bool harvest = dir == HBFS_TOP_DOWN && S.e_f >= A.harvest_min_arcs;
+        const bool harvest = dir == HBFS_TOP_DOWN && SQ.e_f >= A.harvest_min_arcs;
         if (cb) {
-            phase_cb_build(A, S, spare, (int)(L & 1));
+            phase_cb_build(A, SQ, spare, (int)(L & 1));
             grid.sync();
             STAMP(2);
-            if (harvest) phase_cb_run<OffT, true>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
-            else phase_cb_run<OffT, false>(A, S, in, out, ctr, (int)(L & 1), sm, s_pre);
+            if (harvest) phase_cb_run<OffT, true, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
+            else phase_cb_run<OffT, false, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
         } else if (dir == HBFS_TOP_DOWN) {
             if (harvest) {
-                td_prologue(A, S, spare);
+                td_prologue(A, SQ, spare);
                 grid.sync();  // vis now holds the frontier: the expansion tests vis alone
                 STAMP(2);
-                phase_td<OffT, true>(A, S, in, out, spare, ctr, sm);
+                phase_td<OffT, true, PART>(A, SQ, in, out, spare, ctr, sm);
             } else {
-                phase_td<OffT, false>(A, S, in, out, spare, ctr, sm);
+                phase_td<OffT, false, PART>(A, SQ, in, out, spare, ctr, sm);
             }
         }
         if (harvest) {
             grid.sync();
             STAMP(3);
-            phase_harvest(A, out, &ctr->packed, red, (int32_t)L + 1);
+            phase_harvest<OffT, PART>(A, out, &ctr->packed, red, (int32_t)L + 1);
         }
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
+            if (PART) {  // the owned-word tiles do not cover the replicated spare plane
+                const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                for (int64_t w = tid; w < A.nw; w += (int64_t)gridDim.x * blockDim.x)
+                    clear_spare_word(A, S.layer, w);
+            }
             if (SCAN && S.v_f * 64 < A.n)
-                phase_bu<OffT, K, kLaneVecsScan, false>(A, S, in, out, spare, ctr, red, sf);
+                phase_bu<OffT, K, kLaneVecsScan, false, PART>(A, S, in, out, spare, ctr, red, sf);
             else if (S.v_f * A.first1_div >= A.n)
-                phase_bu<OffT, K, kLaneVecs, true>(A, S, in, out, spare, ctr, red, sf);
-            else phase_bu<OffT, K, kLaneVecs, false>(A, S, in, out, spare, ctr, red, sf);
+                phase_bu<OffT, K, kLaneVecs, true, PART>(A, S, in, out, spare, ctr, red, sf);
+            else phase_bu<OffT, K, kLaneVecs, false, PART>(A, S, in, out, spare, ctr, red, sf);
         }
         grid.sync();
 
@@ -1640,6 +1689,152 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     }
     HB_CUDA(cudaStreamSynchronize(st));
     if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, w->ev0, w->ev1));
+    return HBFS_OK;
+}
+
+// ------------------------------------------- partition traversal (PART)
+
+// One rank's share of a 1D partition, traversed one layer per launch of the
+// persistent kernel (bfs_kernel<..., PART = true>); the host loop and the
+// exchange between launches are in csrc/part.cu.
+struct PartTrav {
+    int64_t n = 0, nw = 0, lo = 0, nown = 0, ncs = 0;
+    int cb_ranges = 0, grid = 0;
+    size_t smem = 0;
+    DevBuf bits, q, qo, qr, cs, cbq, cbqo, cbqr, cbcs, ctl, phases;
+    Args<uint64_t> A;
+};
+
+static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 2, true, true>; }
+
+void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
+                       const uint32_t *adj, const uint32_t *posw_local, uint32_t *parent_local,
+                       int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad) {
+    PartTrav *T = new PartTrav();
+    // planes padded to world * (words per rank): the in-place all-gather of a
+    // plane writes exactly that many words
+    const int64_t nw = std::max<int64_t>((n + 31) / 32, nw_pad);
+    T->n = n;
+    T->nw = nw;
+    T->lo = lo;
+    T->nown = nown;
+    T->ncs = arcs_local / kTdChunk + 2;
+    int rc = T->bits.alloc((1 + kPlanes) * nw * 4 + 64);
+    if (!rc) rc = T->q.alloc(2 * (nown + 1) * 4 + 16);
+    if (!rc) rc = T->qo.alloc(2 * (nown + 1) * 8);
+    if (!rc) rc = T->qr.alloc(2 * (nown + 1) * 8);
+    if (!rc) rc = T->cs.alloc(2 * T->ncs * 4);
+    T->cb_ranges = n >= env_i64("HBFS_CB_MIN_N", kCbMinN) ? (int)std::min<int64_t>(31, std::max<int64_t>(2, n >> 22)) : 0;
+    if (!rc && T->cb_ranges) {
+        const int64_t P = T->cb_ranges;
+        rc = T->cbq.alloc(P * kCbMaxF * 4);
+        if (!rc) rc = T->cbqo.alloc(P * kCbMaxF * 8);
+        if (!rc) rc = T->cbqr.alloc(P * kCbMaxF * 8);
+        if (!rc) rc = T->cbcs.alloc(P * T->ncs * 4);
+    }
+    if (!rc) rc = T->ctl.alloc(ctl_bytes());
+    if (!rc) rc = T->phases.alloc((kRowsCap + 1) * kPhaseSlots * 8);
+    if (!rc) {
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        T->smem = dyn_smem_bytes<uint64_t>();
+        cudaError_t e = cudaFuncSetAttribute(part_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T->smem);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, part_kernel(), kBlock, T->smem);
+        if (e != cudaSuccess || per_sm < 1) rc = set_error(HBFS_ECUDA, "occupancy query failed");
+        T->grid = per_sm * sms;
+    }
+    if (rc) {
+        delete T;
+        *rc_out = rc;
+        return nullptr;
+    }
+    Args<uint64_t> &A = T->A;
+    memset(&A, 0, sizeof(A));
+    // vertex- and word-indexed arrays as offset views: global ids index them
+    A.rs = rs_local - lo;
+    A.adj = adj;
+    A.posw = posw_local - (lo >> 5);
+    A.n = n;
+    A.nw = nw;
+    A.arcs = arcs_local;
+    A.ncs = T->ncs;
+    A.parent = parent_local - lo;
+    A.level = level_local - lo;
+    A.bits = T->bits.as<uint32_t>();
+    for (int b = 0; b < 2; ++b) {
+        A.qb[b].q = T->q.as<uint32_t>() + b * (nown + 1);
+        A.qb[b].qo = T->qo.as<uint64_t>() + b * (nown + 1);
+        A.qb[b].qr = T->qr.as<uint64_t>() + b * (nown + 1);
+        A.qb[b].cs = T->cs.as<uint32_t>() + b * T->ncs;
+    }
+    A.cbq.q = T->cbq.as<uint32_t>();
+    A.cbq.qo = T->cbqo.as<uint64_t>();
+    A.cbq.qr = T->cbqr.as<uint64_t>();
+    A.cbq.cs = T->cbcs.as<uint32_t>();
+    A.cb_ranges = T->cb_ranges;
+    A.cb_range_len = T->cb_ranges ? (n + T->cb_ranges - 1) / T->cb_ranges : 0;
+    A.cb_cs_stride = T->ncs;
+    A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
+    A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
+    A.direct_levels = 1;
+    A.first1_div = 0;
+    A.ctl = T->ctl.as<Ctl>();
+    A.rows = reinterpret_cast<hbfs_layer_row *>(T->ctl.as<char>() + sizeof(Ctl));
+    A.rows_cap = 1;
+    A.phase_ns = T->phases.as<unsigned long long>();
+    A.part_w0 = lo >> 5;
+    A.part_wend = (lo >> 5) + (nown + 31) / 32;
+    A.part_lo = lo;
+    A.part_nown = nown;
+    A.cand = cand;
+    A.touch = touch;
+    *rc_out = HBFS_OK;
+    return T;
+}
+
+void part_trav_free(void *h) { delete static_cast<PartTrav *>(h); }
+
+uint32_t *part_trav_plane(void *h, int64_t depth) {
+    PartTrav *T = static_cast<PartTrav *>(h);
+    return depth < 0 ? T->bits.as<uint32_t>() : T->bits.as<uint32_t>() + T->nw * (1 + depth % kPlanes);
+}
+
+// One layer: the global controller state in, this rank's counters out
+// ({found, their degree sum, gathers, fallbacks}); direction = decide(state).
+int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
+                    const hbfs_params *p, unsigned long long counters[4], cudaStream_t st) {
+    PartTrav *T = static_cast<PartTrav *>(h);
+    Args<uint64_t> A = T->A;
+    A.H.heuristic = p->heuristic;
+    A.H.counter_mode = p->counter_mode;
+    A.H.force = p->force_direction;
+    A.H.alpha = p->alpha;
+    A.H.beta = p->beta;
+    A.H.n = T->n;
+    A.max_pos = p->max_pos;
+    A.use_simd = p->use_simd;
+    A.parent_mode = HBFS_PARENT_MINID;
+    A.root = root;
+    A.do_init = do_init;
+    struct {
+        int64_t layer, v_f, e_f, eu_v, eu_e, prev_vf;
+        int32_t dir, kind, done;
+        uint32_t lv_done;
+        int64_t rows;
+        unsigned long long conv;
+    } hs = {state[0], state[1], state[2], state[3], state[4], state[5], dir, 1, 0, 0u, 0, 0ull};
+    static_assert(offsetof(Ctl, conv) + sizeof(unsigned long long) == sizeof(hs), "Ctl head layout");
+    HB_CUDA(cudaMemcpyAsync(A.ctl, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+    void *kargs[] = {&A};
+    HB_CUDA(cudaLaunchCooperativeKernel(part_kernel(), dim3(T->grid), dim3(kBlock), kargs, T->smem, st));
+    Ctr c;
+    HB_CUDA(cudaMemcpyAsync(&c, &A.ctl->ctr[state[0] % 3], sizeof(Ctr), cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    counters[0] = c.packed >> kPackShift;
+    counters[1] = c.packed & kPackMask;
+    counters[2] = c.gathers;
+    counters[3] = c.fallbacks;
     return HBFS_OK;
 }
 

@@ -108,6 +108,16 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st);
 
+// Partition traversal with the persistent kernel, one layer per launch
+// (bfs.cu; driven by the multi-GPU loop in part.cu).
+void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
+                       const uint32_t *adj, const uint32_t *posw_local, uint32_t *parent_local,
+                       int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad);
+void part_trav_free(void *h);
+uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
+int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
+                    const hbfs_params *p, unsigned long long counters[4], cudaStream_t st);
+
 }  // namespace hbfs
 
 struct hbfs_graph {

@@ -55,6 +55,13 @@ struct Part {
     size_t scan_bytes = 0;
     int world = 0;            // partition the queues were sized for
     int64_t span = 0;         // vertices per owner block (word aligned)
+    void *trav = nullptr;     // persistent-kernel traversal state (bfs.cu part_trav_*)
+    DevBuf recs_s, recs_r, acnt;  // records out / in, apply counters
+    DevBuf counts_dev;        // int64[2 * world] record counts sent / received
+    size_t cap_s = 0, cap_r = 0;
+    ~Part() {
+        if (trav) part_trav_free(trav);
+    }
 };
 
 static inline int pgrid(int64_t items, int block = 256) {
@@ -351,6 +358,42 @@ __global__ void kp_td_recv_claim(const unsigned long long *rec, int64_t nrec, in
     }
 }
 
+// Records applied to the persistent kernel's state: every record lowers the
+// owned parent (NIL-initialised; the rank's own arcs did the same in the
+// kernel); the first claim of the next-frontier bit stamps the level and
+// counts the vertex.
+__global__ void kp_apply_persist(const unsigned long long *rec, int64_t nrec, int64_t lo, int32_t depth1,
+                                 const uint64_t *rs, uint32_t *parent, int32_t *level, uint32_t *out_plane,
+                                 unsigned long long *cnt) {
+    unsigned long long c_cnt = 0, c_deg = 0;
+    PSTRIDE(k, nrec) {
+        const unsigned long long r = rec[k];
+        const uint32_t v = (uint32_t)r;
+        const int64_t lv = (int64_t)v - lo;
+        atomicMin(&parent[lv], (uint32_t)(r >> 32));
+        const uint32_t b = 1u << (v & 31);
+        if (atomicOr(&out_plane[v >> 5], b) & b) continue;
+        level[lv] = depth1;
+        c_cnt += 1;
+        c_deg += (unsigned long long)(rs[lv + 1] - rs[lv]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c_cnt += __shfl_down_sync(0xffffffffu, c_cnt, o);
+        c_deg += __shfl_down_sync(0xffffffffu, c_deg, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c_cnt) atomicAdd(&cnt[0], c_cnt);
+        if (c_deg) atomicAdd(&cnt[1], c_deg);
+    }
+}
+
+__global__ void kp_vis_absorb(int64_t W, const uint32_t *plane, uint32_t *vis) {
+    PSTRIDE(w, W) {
+        const uint32_t x = plane[w];
+        if (x) vis[w] |= x;
+    }
+}
+
 __global__ void kp_fill_i32(int32_t *p, int64_t n, int32_t x) {
     PSTRIDE(i, n) p[i] = x;
 }
@@ -629,6 +672,17 @@ extern "C" int hbfs_part_hint_frontier(hbfs_part *P, int64_t v_f) {
     return HBFS_OK;
 }
 
+// Records per owner from the touch bitmap (popcount + scan in vertex order).
+static int td_owner_counts(Part *P, int world, int64_t wper, int64_t *send_counts, cudaStream_t st) {
+    uint32_t *cnt = P->wcnt.as<uint32_t>();
+    kp_touch_popc<<<pgrid(P->W + 1), 256, 0, st>>>(P->W, P->touch.as<uint32_t>(), cnt);
+    size_t tb = P->scan_bytes;
+    HB_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, tb, cnt, P->wexcl.as<uint32_t>(), (int)(P->W + 1), st));
+    kp_owner_counts<<<1, 32, 0, st>>>(world, wper, P->W, P->wexcl.as<uint32_t>(), send_counts);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+}
+
 // Top-down expansion of the owned frontier for a `world`-rank partition (owner
 // blocks of `span` = partition() words * 32 vertices).  send_counts: device
 // int64[world], records queued per owner.
@@ -659,12 +713,7 @@ extern "C" int hbfs_part_td_expand(hbfs_part *P, int32_t world, int64_t *send_co
                                    P->V.as<uint32_t>(), P->cand.as<int32_t>(), P->touch.as<uint32_t>(),
                                    P->seg_u.as<uint32_t>(), P->seg_k.as<uint64_t>(), qn + 1,
                                    P->pieces.as<Piece>(), rcur + P->ranges);
-    uint32_t *cnt = P->wcnt.as<uint32_t>();
-    kp_touch_popc<<<pgrid(P->W + 1), 256, 0, st>>>(P->W, P->touch.as<uint32_t>(), cnt);
-    size_t tb = P->scan_bytes;
-    HB_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, tb, cnt, P->wexcl.as<uint32_t>(), (int)(P->W + 1), st));
-    kp_owner_counts<<<1, 32, 0, st>>>(world, wper, P->W, P->wexcl.as<uint32_t>(), send_counts);
-    HB_CUDA(cudaGetLastError());
+    HB_CHECK(td_owner_counts(P, world, wper, send_counts, st));
     return HBFS_OK;
     HB_ENTRY_END
 }
@@ -871,93 +920,178 @@ int grow(hbfs::DevBuf &b, size_t &cap, size_t need) {
 }
 }  // namespace
 
-extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_params *p,
-                           hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers,
-                           float *device_ms, void *stream) {
-    HB_ENTRY_BEGIN
-    clear_error();
-    if (!M || !P || !p) return set_error(HBFS_EINVAL, "null argument");
-    if (root < 0 || root >= P->n)
-        return set_error(HBFS_ERANGE, "source %lld out of range [0, %lld)", (long long)root, (long long)P->n);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int world = M->world, rank = M->rank;
-    const int64_t wper = (P->W + world - 1) / world;
-    if (P->lo != rank * wper * 32) return set_error(HBFS_EINVAL, "partition does not match rank/world");
-    if (!M->next_full.p || M->next_full.bytes < (size_t)(wper * world * 4))
-        HB_CHECK(M->next_full.alloc(wper * world * 4 + 16));
-    uint32_t *next_full = M->next_full.as<uint32_t>();
-    uint32_t *slice = next_full + rank * wper;
-    unsigned long long *ctr = M->ctr.as<unsigned long long>();
-    int64_t *sc = M->counts.as<int64_t>(), *rcv = sc + world;
-    int64_t *scal = M->scal.as<int64_t>();
+// The per-layer loop over the persistent partition kernel (bfs.cu
+// part_trav_layer).  Either one part per process with NCCL (M != nullptr),
+// or all `world` parts of a partition in this process on one device (M ==
+// nullptr: exchanges are device copies; used to test P ranks on one GPU).
+static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64_t root,
+                        const hbfs_params *p, hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers,
+                        float *device_ms, cudaStream_t st) {
+    if (p->parent_mode != HBFS_PARENT_MINID) return set_error(HBFS_EINVAL, "partitions use min-id parents");
+    Part *P0 = Ps[0];
+    const int64_t n = P0->n, W = P0->W;
+    const int64_t wper = (W + world - 1) / world, nw_pad = wper * world;
+    for (int i = 0; i < nparts; ++i) {
+        Part *P = Ps[i];
+        const int rank = M ? M->rank : i;
+        if (P->n != n || P->lo != rank * wper * 32) return set_error(HBFS_EINVAL, "partition does not match rank/world");
+        if (!P->trav) {
+            int rc = HBFS_OK;
+            P->trav = part_trav_create(n, P->lo, P->nloc, P->arcs, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
+                                       P->posw.as<uint32_t>(), P->parent.as<uint32_t>(), P->level.as<int32_t>(),
+                                       reinterpret_cast<uint32_t *>(P->cand.as<int32_t>()), P->touch.as<uint32_t>(),
+                                       &rc, nw_pad);
+            if (!P->trav) return rc;
+        }
+        if (!P->acnt.p) HB_CHECK(P->acnt.alloc(64));
+        if (!P->counts_dev.p) HB_CHECK(P->counts_dev.alloc(16 * world + 16));
+    }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    HB_CUDA(cudaEventCreate(&ev0));
+    HB_CUDA(cudaEventCreate(&ev1));
+    HB_CUDA(cudaEventRecord(ev0, st));
+    // root degree and global arc count
+    int64_t h2[2] = {0, 0};
+    for (int i = 0; i < nparts; ++i) {
+        int64_t d = 0;
+        if (root >= Ps[i]->lo && root < Ps[i]->hi) HB_CHECK(hbfs_part_degree(Ps[i], root, &d));
+        h2[0] += d;
+        h2[1] += Ps[i]->arcs;
+    }
+    if (M) {
+        int64_t *scal = M->scal.as<int64_t>();
+        HB_CUDA(cudaMemcpyAsync(scal, h2, 16, cudaMemcpyHostToDevice, st));
+        HB_NCCL(nccl().allReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
+        HB_CUDA(cudaMemcpyAsync(h2, scal, 16, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+    }
     Heur H;
     H.heuristic = p->heuristic;
     H.counter_mode = p->counter_mode;
     H.force = p->force_direction;
     H.alpha = p->alpha;
     H.beta = p->beta;
-    H.n = P->n;
-
-    HB_CUDA(cudaEventRecord(M->ev0, st));
-    HB_CHECK(hbfs_part_init(P, root, st));
-    // root degree and the global arc count: one all-reduce
-    int64_t h2[2] = {0, P->arcs};
-    if (root >= P->lo && root < P->hi) HB_CHECK(hbfs_part_degree(P, root, &h2[0]));
-    HB_CUDA(cudaMemcpyAsync(scal, h2, 16, cudaMemcpyHostToDevice, st));
-    HB_NCCL(nccl().allReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
-    HB_CUDA(cudaMemcpyAsync(h2, scal, 16, cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaStreamSynchronize(st));
-    const int64_t rdeg = h2[0], arcs_global = h2[1];
-    int64_t v_f = 1, e_f = rdeg, eu_v = P->n - 1, eu_e = arcs_global - rdeg, prev_vf = 0;
+    H.n = n;
+    int64_t v_f = 1, e_f = h2[0], eu_v = n - 1, eu_e = h2[1] - h2[0], prev_vf = 0, layer = 0;
     int cur = HBFS_TOP_DOWN;
-    int64_t layer = 0;
-    std::vector<int64_t> hc(2 * world);
+    std::vector<int64_t> hc((size_t)2 * world * nparts);  // [part][send world | recv world]
     while (v_f > 0) {
         int64_t fv, gv;
         const int d = decide(H, cur, v_f, e_f, eu_v, eu_e, prev_vf, &fv, &gv);
-        HB_CUDA(cudaMemsetAsync(slice, 0, wper * 4, st));
-        if (d == HBFS_BOTTOM_UP) {
-            P->fhint = v_f;
-            HB_CHECK(hbfs_part_bu(P, (int32_t)layer, p->max_pos, slice, ctr, st));
-        } else {
-            HB_CHECK(hbfs_part_td_expand(P, world, sc, st));
-            HB_NCCL(nccl().groupStart());
-            for (int r = 0; r < world; ++r) {
-                HB_NCCL(nccl().send(sc + r, 1, ncclInt64, r, M->comm, st));
-                HB_NCCL(nccl().recv(rcv + r, 1, ncclInt64, r, M->comm, st));
+        const int64_t state[6] = {layer, v_f, e_f, eu_v, eu_e, prev_vf};
+        unsigned long long tot[4] = {0, 0, 0, 0};
+        for (int i = 0; i < nparts; ++i) {
+            unsigned long long c[4];
+            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, c, st));
+            for (int k = 0; k < 4; ++k) tot[k] += c[k];
+        }
+        if (d == HBFS_TOP_DOWN) {
+            for (int i = 0; i < nparts; ++i)
+                HB_CHECK(td_owner_counts(Ps[i], world, wper, Ps[i]->counts_dev.as<int64_t>(), st));
+            if (M) {
+                int64_t *sc = Ps[0]->counts_dev.as<int64_t>(), *rc = sc + world;
+                HB_NCCL(nccl().groupStart());
+                for (int r = 0; r < world; ++r) {
+                    HB_NCCL(nccl().send(sc + r, 1, ncclInt64, r, M->comm, st));
+                    HB_NCCL(nccl().recv(rc + r, 1, ncclInt64, r, M->comm, st));
+                }
+                HB_NCCL(nccl().groupEnd());
+                HB_CUDA(cudaMemcpyAsync(hc.data(), sc, 16 * world, cudaMemcpyDeviceToHost, st));
+            } else {
+                for (int i = 0; i < nparts; ++i)
+                    HB_CUDA(cudaMemcpyAsync(hc.data() + (size_t)2 * world * i, Ps[i]->counts_dev.p, 8 * world,
+                                            cudaMemcpyDeviceToHost, st));
             }
-            HB_NCCL(nccl().groupEnd());
-            HB_CUDA(cudaMemcpyAsync(hc.data(), sc, 16 * world, cudaMemcpyDeviceToHost, st));
             HB_CUDA(cudaStreamSynchronize(st));
-            int64_t ns = 0, nr = 0;
-            for (int r = 0; r < world; ++r) {
-                ns += hc[r];
-                nr += hc[world + r];
+            if (!M)  // recv[i][s] = send[s][i]
+                for (int i = 0; i < nparts; ++i)
+                    for (int sr = 0; sr < world; ++sr) hc[(size_t)2 * world * i + world + sr] = hc[(size_t)2 * world * sr + i];
+            for (int i = 0; i < nparts; ++i) {
+                Part *P = Ps[i];
+                int64_t ns = 0, nr = 0;
+                for (int r = 0; r < world; ++r) {
+                    ns += hc[(size_t)2 * world * i + r];
+                    nr += hc[(size_t)2 * world * i + world + r];
+                }
+                if ((size_t)ns + 1 > P->cap_s) {
+                    HB_CHECK(P->recs_s.alloc((ns + ns / 4 + 1024) * 8));
+                    P->cap_s = ns + ns / 4 + 1024;
+                }
+                if ((size_t)nr + 1 > P->cap_r) {
+                    HB_CHECK(P->recs_r.alloc((nr + nr / 4 + 1024) * 8));
+                    P->cap_r = nr + nr / 4 + 1024;
+                }
+                kp_td_pack<<<pgrid(P->W), 256, 0, st>>>(P->W, P->wexcl.as<uint32_t>(), P->cand.as<int32_t>(),
+                                                        P->touch.as<uint32_t>(), P->recs_s.as<unsigned long long>());
+                HB_CUDA(cudaGetLastError());
             }
-            HB_CHECK(grow(M->recs_s, M->cap_s, (size_t)ns));
-            HB_CHECK(grow(M->recs_r, M->cap_r, (size_t)nr));
-            HB_CHECK(hbfs_part_td_pack(P, M->recs_s.as<uint64_t>(), st));
-            uint64_t *rs_ = M->recs_s.as<uint64_t>(), *rr_ = M->recs_r.as<uint64_t>();
-            HB_NCCL(nccl().groupStart());
-            {
+            if (M) {
+                const int64_t *h = hc.data();
+                HB_NCCL(nccl().groupStart());
                 int64_t os = 0, orr = 0;
                 for (int r = 0; r < world; ++r) {
-                    if (hc[r]) HB_NCCL(nccl().send(rs_ + os, (size_t)hc[r], ncclUint64, r, M->comm, st));
-                    if (hc[world + r]) HB_NCCL(nccl().recv(rr_ + orr, (size_t)hc[world + r], ncclUint64, r, M->comm, st));
-                    os += hc[r];
-                    orr += hc[world + r];
+                    if (h[r]) HB_NCCL(nccl().send(Ps[0]->recs_s.as<uint64_t>() + os, (size_t)h[r], ncclUint64, r, M->comm, st));
+                    if (h[world + r])
+                        HB_NCCL(nccl().recv(Ps[0]->recs_r.as<uint64_t>() + orr, (size_t)h[world + r], ncclUint64, r, M->comm, st));
+                    os += h[r];
+                    orr += h[world + r];
+                }
+                HB_NCCL(nccl().groupEnd());
+            } else {
+                for (int i = 0; i < nparts; ++i) {  // receiver i gathers sender segments in rank order
+                    int64_t orr = 0;
+                    for (int sr = 0; sr < nparts; ++sr) {
+                        int64_t os = 0;
+                        for (int r = 0; r < i; ++r) os += hc[(size_t)2 * world * sr + r];
+                        const int64_t c = hc[(size_t)2 * world * sr + i];
+                        if (c)
+                            HB_CUDA(cudaMemcpyAsync(Ps[i]->recs_r.as<uint64_t>() + orr, Ps[sr]->recs_s.as<uint64_t>() + os,
+                                                    c * 8, cudaMemcpyDeviceToDevice, st));
+                        orr += c;
+                    }
                 }
             }
-            HB_NCCL(nccl().groupEnd());
-            HB_CHECK(hbfs_part_td_apply(P, (int32_t)layer, rr_, nr, slice, ctr, st));
+            for (int i = 0; i < nparts; ++i) {
+                Part *P = Ps[i];
+                int64_t nr = 0;
+                for (int r = 0; r < world; ++r) nr += hc[(size_t)2 * world * i + world + r];
+                HB_CUDA(cudaMemsetAsync(P->acnt.p, 0, 16, st));
+                if (nr)
+                    kp_apply_persist<<<pgrid(nr), 256, 0, st>>>(P->recs_r.as<unsigned long long>(), nr, P->lo,
+                                                               (int32_t)layer + 1, P->rs.as<uint64_t>(),
+                                                               P->parent.as<uint32_t>(), P->level.as<int32_t>(),
+                                                               part_trav_plane(P->trav, layer + 1),
+                                                               P->acnt.as<unsigned long long>());
+                unsigned long long ac[2];
+                HB_CUDA(cudaMemcpyAsync(ac, P->acnt.p, 16, cudaMemcpyDeviceToHost, st));
+                HB_CUDA(cudaStreamSynchronize(st));
+                tot[0] += ac[0];
+                tot[1] += ac[1];
+            }
         }
-        HB_NCCL(nccl().allGather(slice, next_full, (size_t)wper, ncclUint32, M->comm, st));
-        HB_NCCL(nccl().allReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
-        HB_CHECK(hbfs_part_absorb(P, next_full, st));
-        unsigned long long c4[4];
-        HB_CUDA(cudaMemcpyAsync(c4, ctr, 32, cudaMemcpyDeviceToHost, st));
-        HB_CUDA(cudaStreamSynchronize(st));
-        const int64_t nvf = (int64_t)c4[0], nef = (int64_t)c4[1];
+        // next frontier: every rank's owned words of plane layer+1 to everyone
+        if (M) {
+            uint32_t *pl = part_trav_plane(Ps[0]->trav, layer + 1);
+            HB_NCCL(nccl().allGather(pl + M->rank * wper, pl, (size_t)wper, ncclUint32, M->comm, st));
+        } else {
+            for (int i = 0; i < nparts; ++i)
+                for (int sr = 0; sr < nparts; ++sr)
+                    if (sr != i)
+                        HB_CUDA(cudaMemcpyAsync(part_trav_plane(Ps[i]->trav, layer + 1) + sr * wper,
+                                                part_trav_plane(Ps[sr]->trav, layer + 1) + sr * wper, wper * 4,
+                                                cudaMemcpyDeviceToDevice, st));
+        }
+        for (int i = 0; i < nparts; ++i)
+            kp_vis_absorb<<<pgrid(nw_pad), 256, 0, st>>>(nw_pad, part_trav_plane(Ps[i]->trav, layer + 1),
+                                                        part_trav_plane(Ps[i]->trav, -1));
+        HB_CUDA(cudaGetLastError());
+        if (M) {
+            unsigned long long *ctr = M->ctr.as<unsigned long long>();
+            HB_CUDA(cudaMemcpyAsync(ctr, tot, 32, cudaMemcpyHostToDevice, st));
+            HB_NCCL(nccl().allReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
+            HB_CUDA(cudaMemcpyAsync(tot, ctr, 32, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+        }
         if (trace && layer < trace_cap) {
             hbfs_layer_row &r = trace[layer];
             r.layer = (int32_t)(layer + 1);
@@ -967,30 +1101,54 @@ extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_pa
             r.e_u = p->counter_mode ? eu_e : eu_v;
             r.f_value = fv;
             r.g_value = gv;
-            if (!p->use_simd) {
-                r.fallback_count = 0;
-                r.gather_count = 0;
-            } else if (d == HBFS_TOP_DOWN) {
-                r.fallback_count = 0;
-                r.gather_count = e_f;
-            } else {
-                r.fallback_count = (int64_t)c4[3];
-                r.gather_count = (int64_t)c4[2];
-            }
+            r.fallback_count = !p->use_simd || d == HBFS_TOP_DOWN ? 0 : (int64_t)tot[3];
+            r.gather_count = !p->use_simd ? 0 : d == HBFS_TOP_DOWN ? e_f : (int64_t)tot[2];
             r.elapsed = 0.0;
         }
         prev_vf = v_f;
-        v_f = nvf;
-        e_f = nef;
-        eu_v -= nvf;
-        eu_e -= nef;
+        v_f = (int64_t)tot[0];
+        e_f = (int64_t)tot[1];
+        eu_v -= v_f;
+        eu_e -= e_f;
         cur = d;
         ++layer;
     }
-    HB_CUDA(cudaEventRecord(M->ev1, st));
-    HB_CUDA(cudaEventSynchronize(M->ev1));
-    if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, M->ev0, M->ev1));
+    HB_CUDA(cudaEventRecord(ev1, st));
+    HB_CUDA(cudaEventSynchronize(ev1));
+    if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (n_layers) *n_layers = layer;
     return HBFS_OK;
+}
+
+extern "C" int hbfs_mg_bfs(hbfs_mg *M, hbfs_part *P, int64_t root, const hbfs_params *p,
+                           hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers,
+                           float *device_ms, void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!M || !P || !p) return set_error(HBFS_EINVAL, "null argument");
+    if (root < 0 || root >= P->n)
+        return set_error(HBFS_ERANGE, "source %lld out of range [0, %lld)", (long long)root, (long long)P->n);
+    hbfs_part *ps[1] = {P};
+    return persist_loop(ps, 1, M, M->world, root, p, trace, trace_cap, n_layers, device_ms,
+                        static_cast<cudaStream_t>(stream));
+    HB_ENTRY_END
+}
+
+// All `world` parts of a partition in this process (one device): the same
+// loop with device copies for the exchanges (tests P ranks on one GPU).
+extern "C" int hbfs_mgl_bfs(hbfs_part **parts, int32_t world, int64_t root, const hbfs_params *p,
+                            hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers, float *device_ms,
+                            void *stream) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!parts || world < 1 || !p) return set_error(HBFS_EINVAL, "bad arguments");
+    for (int i = 0; i < world; ++i)
+        if (!parts[i]) return set_error(HBFS_EINVAL, "null part");
+    if (root < 0 || root >= parts[0]->n)
+        return set_error(HBFS_ERANGE, "source %lld out of range [0, %lld)", (long long)root, (long long)parts[0]->n);
+    return persist_loop(parts, world, nullptr, world, root, p, trace, trace_cap, n_layers, device_ms,
+                        static_cast<cudaStream_t>(stream));
     HB_ENTRY_END
 }

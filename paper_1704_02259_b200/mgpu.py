@@ -540,3 +540,39 @@ def run_benchmark_distributed(params, mode: str = "simd-hybrid", heuristic: Heur
                            harmonic_mean_teps=harmonic_mean(positive) if positive else 0.0,
                            min_seconds=min(secs), max_seconds=max(secs), mean_seconds=sum(secs) / len(secs),
                            zero_teps_runs=len(results) - len(positive), teps_denominator=m)
+
+
+class LocalPersistBfs:
+    """All P ranks of a partition in this process on one GPU, through the C++
+    loop over the persistent partition kernel (``hbfs_mgl_bfs``): the exchange
+    steps are device copies.  Tests the multi-GPU kernel path on one GPU."""
+
+    def __init__(self, ranks):
+        from . import _lib
+
+        self._lib = _lib
+        self.ranks = list(ranks)
+        self.lib = self.ranks[0].lib
+        self._handles = (C.c_void_p * len(self.ranks))(*[r.h for r in self.ranks])
+        self._rows = (_lib.hbfs_layer_row * 4096)()
+
+    def bfs(self, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = None,
+            use_simd: bool = True, force_direction=None) -> DistResult:
+        from .hybrid import _params
+
+        p = p if p is not None else HeuristicParams()
+        cfg = cfg if cfg is not None else VecConfig()
+        hp = _params(p, cfg, use_simd, force_direction, "minid")
+        nl, ms = C.c_int64(), C.c_float()
+        self._lib.check(self.lib.hbfs_mgl_bfs(self._handles, len(self.ranks), int(root), C.byref(hp), self._rows,
+                                              len(self._rows), C.byref(nl), C.byref(ms), self._lib.current_stream()))
+        kern = "simd" if use_simd else "scalar"
+        trace = [LayerTraceRow(layer=r.layer, direction=BOTTOM_UP if r.direction else TOP_DOWN, kernel=kern,
+                               v_f=r.v_f, e_f=r.e_f, e_u=r.e_u, f_value=r.f_value, g_value=r.g_value,
+                               elapsed=r.elapsed, fallback_count=r.fallback_count,
+                               gather_count=r.gather_count)
+                 for r in self._rows[: min(nl.value, len(self._rows))]]
+        return DistResult(trace=trace, seconds=ms.value * 1e-3)
+
+    def outputs(self):
+        return [r.outputs() for r in self.ranks]

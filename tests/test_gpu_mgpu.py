@@ -87,3 +87,53 @@ def test_nccl_loop_single_rank(cuda, small_golden, name):
             assert np.array_equal(par, small_golden[f"{name}/{s}/{mode}/parent"]), (name, s, mode)
             assert np.array_equal(trace_array(res.trace), small_golden[f"{name}/{s}/{mode}/trace"]), (name, s, mode)
     nb.free()
+
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("name", ["k8", "k10", "u12"])
+def test_persistent_partition_kernel(cuda, small_golden, world, name):
+    """P ranks of the persistent partition kernel (one launch per layer, the
+    C++ loop with device-copy exchanges) on one GPU: levels, min-id parents and
+    the trace equal the reference's."""
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, LocalPersistBfs
+
+    rs, adj = small_golden[f"{name}/rs"], small_golden[f"{name}/adj"]
+    ranks = [CudaRankOps.from_csr(rs, adj, len(adj) // 2, world, r) for r in range(world)]
+    lb = LocalPersistBfs(ranks)
+    for s in small_golden[f"{name}/sources"][:4]:
+        s = int(s)
+        for mode, kw in MODES.items():
+            p = hb.HeuristicParams(**kw.get("p", {}))
+            res = lb.bfs(s, p, use_simd=kw["use_simd"], force_direction=kw.get("force_direction"))
+            outs = lb.outputs()
+            par = np.concatenate([o[0] for o in outs])
+            lev = np.concatenate([o[1] for o in outs])
+            assert np.array_equal(lev, small_golden[f"{name}/{s}/level"]), (name, world, s, mode)
+            assert np.array_equal(par, small_golden[f"{name}/{s}/{mode}/parent"]), (name, world, s, mode)
+            assert np.array_equal(trace_array(res.trace), small_golden[f"{name}/{s}/{mode}/trace"]), (name, world, s, mode)
+
+
+def test_persistent_partition_large(cuda, monkeypatch):
+    """The large-graph paths (column-blocked and harvest top-down) forced on a
+    SCALE 14 graph, P = 1, 2, 4, against the single-GPU traversal."""
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, LocalPersistBfs
+
+    monkeypatch.setenv("HBFS_CB_MIN_N", "1024")
+    monkeypatch.setenv("HBFS_CB_MIN_ARCS", "256")
+    monkeypatch.setenv("HBFS_HARVEST_MIN_ARCS", "4096")
+    params = hb.GraphParams(scale=14, edgefactor=16, seed=1)
+    g = hb.generate_graph(params)
+    roots = hb.sample_sources(g, 6, 1)
+    p = hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge")
+    for world in (1, 2, 4):
+        lb = LocalPersistBfs([CudaRankOps.generate(params, world, r) for r in range(world)])
+        for s in roots:
+            ref = hb.bfs(g, int(s), p, device=False)
+            res = lb.bfs(int(s), p)
+            outs = lb.outputs()
+            assert np.array_equal(np.concatenate([o[1] for o in outs]), ref.level), (world, s)
+            assert np.array_equal(np.concatenate([o[0] for o in outs]), ref.parent), (world, s)
+            assert [r.direction for r in res.trace] == [r.direction for r in ref.trace]

@@ -7,13 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_1704_02259_b200 as hb
-from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm, NcclBfs
+from paper_1704_02259_b200.mgpu import CudaRankOps, DistBfs, LocalComm, LocalPersistBfs, NcclBfs
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--roots", type=int, default=8)
 ap.add_argument("--ranks", default="1,2,4")
 ap.add_argument("--layers", action="store_true")
+ap.add_argument("--persist", action="store_true", help="P ranks through the persistent partition kernel (C++ loop)")
 a = ap.parse_args()
 params = hb.GraphParams(scale=a.scale, edgefactor=16, seed=1)
 g = hb.generate_graph(params)
@@ -29,7 +30,7 @@ ref = {int(s): hb.bfs(g, int(s), p, device=False) for s in roots[:2]}
 g.free()
 for P in [int(x) for x in a.ranks.split(",")]:
     ranks = [CudaRankOps.generate(params, P, r) for r in range(P)]
-    db = DistBfs(ranks, LocalComm(P))
+    db = LocalPersistBfs(ranks) if a.persist else DistBfs(ranks, LocalComm(P))
     db.bfs(int(roots[0]), p)
     ts = []
     for s in roots:
