@@ -585,13 +585,22 @@ __device__ void phase_init(const Args<OffT> &A) {
 // :207-239).
 // Prologue of every top-down layer: clear the spare bitmap; in min-id mode
 // commit the frontier to vis (the arc tests use vis | in, so no barrier).
-template <typename OffT>
+template <typename OffT, bool PART = false>
 __device__ void td_prologue(const Args<OffT> &A, const St &S, const Plane spare) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Plane vis{A.bits};
-    for (int64_t w = tid; w < A.nw; w += nth) clear_spare_word(A, S.layer, w);
+    if (PART) {  // also: the all-gathered frontier joins the replicated visited bitmap
+        const Plane in = depth_plane(A, S.layer);
+        for (int64_t w = tid; w < A.nw; w += nth) {
+            clear_spare_word(A, S.layer, w);
+            const uint32_t x = in[w];
+            if (x && (vis[w] & x) != x) vis[w] |= x;
+        }
+    } else {
+        for (int64_t w = tid; w < A.nw; w += nth) clear_spare_word(A, S.layer, w);
+    }
     if (A.parent_mode != HBFS_PARENT_ANY) {
         for (int64_t i = tid; i < S.v_f; i += nth) {
             const uint32_t x = Q.q[i];
@@ -748,7 +757,7 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
                          const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
-    if (!Harvest) td_prologue(A, S, spare);  // harvest layers run it before a barrier
+    if (!Harvest) td_prologue<OffT, PART>(A, S, spare);  // harvest layers run it before a barrier
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
     constexpr int SPAN = Harvest ? 2 : 1;
@@ -776,13 +785,13 @@ __device__ __forceinline__ Queue<OffT> cb_queue(const Args<OffT> &A, int r, int6
 // Column-blocked top-down, phase A: split every frontier row into cb_ranges
 // sub-rows by target id (rows are sorted, so each is a contiguous segment
 // found by binary search) and append the segments to per-range queues.
-template <typename OffT>
+template <typename OffT, bool PART = false>
 __device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spare, int bank) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     const Queue<OffT> &Q = A.qb[S.layer & 1];
-    td_prologue(A, S, spare);
+    td_prologue<OffT, PART>(A, S, spare);
     const int P = A.cb_ranges;
     const int64_t nf = S.v_f;
     const uint64_t mf = (uint64_t)S.e_f;
@@ -1307,14 +1316,14 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         }
         const bool harvest = dir == HBFS_TOP_DOWN && SQ.e_f >= A.harvest_min_arcs;
         if (cb) {
-            phase_cb_build(A, SQ, spare, (int)(L & 1));
+            phase_cb_build<OffT, PART>(A, SQ, spare, (int)(L & 1));
             grid.sync();
             STAMP(2);
             if (harvest) phase_cb_run<OffT, true, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
             else phase_cb_run<OffT, false, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
         } else if (dir == HBFS_TOP_DOWN) {
             if (harvest) {
-                td_prologue(A, SQ, spare);
+                td_prologue<OffT, PART>(A, SQ, spare);
                 grid.sync();  // vis now holds the frontier: the expansion tests vis alone
                 STAMP(2);
                 phase_td<OffT, true, PART>(A, SQ, in, out, spare, ctr, sm);
@@ -1329,10 +1338,17 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         }
         if (dir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
-            if (PART) {  // the owned-word tiles do not cover the replicated spare plane
+            const Plane vis_all{A.bits};
+            if (PART) {  // the owned-word tiles do not cover the replicated planes:
+                // clear the spare plane; absorb the all-gathered frontier into
+                // the other ranks' words of vis (owned words: phase_bu's commit)
                 const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-                for (int64_t w = tid; w < A.nw; w += (int64_t)gridDim.x * blockDim.x)
+                for (int64_t w = tid; w < A.nw; w += (int64_t)gridDim.x * blockDim.x) {
                     clear_spare_word(A, S.layer, w);
+                    if (w >= A.part_w0 && w < A.part_wend) continue;
+                    const uint32_t x = in[w];
+                    if (x && (vis_all[w] & x) != x) vis_all[w] |= x;
+                }
             }
             if (SCAN && S.v_f * 64 < A.n)
                 phase_bu<OffT, K, kLaneVecsScan, false, PART>(A, S, in, out, spare, ctr, red, sf);
@@ -1703,6 +1719,10 @@ struct PartTrav {
     size_t smem = 0;
     DevBuf bits, q, qo, qr, cs, cbq, cbqo, cbqr, cbcs, ctl, phases;
     Args<uint64_t> A;
+    Ctr *h_ctr = nullptr;  // pinned: the last layer's counters (valid after a stream sync)
+    ~PartTrav() {
+        if (h_ctr) cudaFreeHost(h_ctr);
+    }
 };
 
 static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 2, true, true>; }
@@ -1734,6 +1754,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     }
     if (!rc) rc = T->ctl.alloc(ctl_bytes());
     if (!rc) rc = T->phases.alloc((kRowsCap + 1) * kPhaseSlots * 8);
+    if (!rc && cudaMallocHost(&T->h_ctr, sizeof(Ctr)) != cudaSuccess) rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
     if (!rc) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
@@ -1800,10 +1821,20 @@ uint32_t *part_trav_plane(void *h, int64_t depth) {
     return depth < 0 ? T->bits.as<uint32_t>() : T->bits.as<uint32_t>() + T->nw * (1 + depth % kPlanes);
 }
 
-// One layer: the global controller state in, this rank's counters out
-// ({found, their degree sum, gathers, fallbacks}); direction = decide(state).
+// One layer, asynchronous: the global controller state in; this rank's
+// counters ({found, their degree sum, gathers, fallbacks}) from
+// part_trav_counters once the stream has been synchronised; direction =
+// decide(state).
+void part_trav_counters(void *h, unsigned long long counters[4]) {
+    const Ctr &c = *static_cast<PartTrav *>(h)->h_ctr;
+    counters[0] = c.packed >> kPackShift;
+    counters[1] = c.packed & kPackMask;
+    counters[2] = c.gathers;
+    counters[3] = c.fallbacks;
+}
+
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, unsigned long long counters[4], cudaStream_t st) {
+                    const hbfs_params *p, cudaStream_t st) {
     PartTrav *T = static_cast<PartTrav *>(h);
     Args<uint64_t> A = T->A;
     A.H.heuristic = p->heuristic;
@@ -1828,13 +1859,7 @@ int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, u
     HB_CUDA(cudaMemcpyAsync(A.ctl, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
     void *kargs[] = {&A};
     HB_CUDA(cudaLaunchCooperativeKernel(part_kernel(), dim3(T->grid), dim3(kBlock), kargs, T->smem, st));
-    Ctr c;
-    HB_CUDA(cudaMemcpyAsync(&c, &A.ctl->ctr[state[0] % 3], sizeof(Ctr), cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaStreamSynchronize(st));
-    counters[0] = c.packed >> kPackShift;
-    counters[1] = c.packed & kPackMask;
-    counters[2] = c.gathers;
-    counters[3] = c.fallbacks;
+    HB_CUDA(cudaMemcpyAsync(T->h_ctr, &A.ctl->ctr[state[0] % 3], sizeof(Ctr), cudaMemcpyDeviceToHost, st));
     return HBFS_OK;
 }
 

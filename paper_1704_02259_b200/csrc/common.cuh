@@ -116,7 +116,8 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
 void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, unsigned long long counters[4], cudaStream_t st);
+                    const hbfs_params *p, cudaStream_t st);  // asynchronous
+void part_trav_counters(void *h, unsigned long long counters[4]);  // after a stream sync
 
 }  // namespace hbfs
 

@@ -58,9 +58,11 @@ struct Part {
     void *trav = nullptr;     // persistent-kernel traversal state (bfs.cu part_trav_*)
     DevBuf recs_s, recs_r, acnt;  // records out / in, apply counters
     DevBuf counts_dev;        // int64[2 * world] record counts sent / received
+    unsigned long long *h_acnt = nullptr;  // pinned: apply counters of the last layer
     size_t cap_s = 0, cap_r = 0;
     ~Part() {
         if (trav) part_trav_free(trav);
+        if (h_acnt) cudaFreeHost(h_acnt);
     }
 };
 
@@ -387,12 +389,6 @@ __global__ void kp_apply_persist(const unsigned long long *rec, int64_t nrec, in
     }
 }
 
-__global__ void kp_vis_absorb(int64_t W, const uint32_t *plane, uint32_t *vis) {
-    PSTRIDE(w, W) {
-        const uint32_t x = plane[w];
-        if (x) vis[w] |= x;
-    }
-}
 
 __global__ void kp_fill_i32(int32_t *p, int64_t n, int32_t x) {
     PSTRIDE(i, n) p[i] = x;
@@ -789,6 +785,7 @@ extern "C" int hbfs_part_outputs(hbfs_part *P, uint32_t *parent, int32_t *level,
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <vector>
 
 // NCCL is resolved at first use (dlopen by SONAME), not linked: the process
@@ -943,7 +940,20 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                        &rc, nw_pad);
             if (!P->trav) return rc;
         }
+        // record buffers at their bounds (a rank sends at most one record per
+        // non-owned vertex and receives at most world-1 per owned vertex, both
+        // <= n): growing them inside a traversal costs milliseconds
+        if (P->cap_s < (size_t)n + 1) {
+            HB_CHECK(P->recs_s.alloc((n + 1) * 8));
+            P->cap_s = n + 1;
+        }
+        if (P->cap_r < (size_t)n + 1) {
+            HB_CHECK(P->recs_r.alloc((n + 1) * 8));
+            P->cap_r = n + 1;
+        }
         if (!P->acnt.p) HB_CHECK(P->acnt.alloc(64));
+        if (!P->h_acnt && cudaMallocHost(&P->h_acnt, 16) != cudaSuccess)
+            return set_error(HBFS_ECUDA, "cudaMallocHost failed");
         if (!P->counts_dev.p) HB_CHECK(P->counts_dev.alloc(16 * world + 16));
     }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -975,16 +985,24 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
     int64_t v_f = 1, e_f = h2[0], eu_v = n - 1, eu_e = h2[1] - h2[0], prev_vf = 0, layer = 0;
     int cur = HBFS_TOP_DOWN;
     std::vector<int64_t> hc((size_t)2 * world * nparts);  // [part][send world | recv world]
+    auto t_layer = std::chrono::steady_clock::now();
     while (v_f > 0) {
         int64_t fv, gv;
         const int d = decide(H, cur, v_f, e_f, eu_v, eu_e, prev_vf, &fv, &gv);
         const int64_t state[6] = {layer, v_f, e_f, eu_v, eu_e, prev_vf};
         unsigned long long tot[4] = {0, 0, 0, 0};
-        for (int i = 0; i < nparts; ++i) {
-            unsigned long long c[4];
-            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, c, st));
-            for (int k = 0; k < 4; ++k) tot[k] += c[k];
-        }
+        for (int i = 0; i < nparts; ++i)  // asynchronous; counters read after the next sync
+            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, st));
+        bool have_ctr = false;
+        auto add_trav_counters = [&]() {
+            if (have_ctr) return;
+            for (int i = 0; i < nparts; ++i) {
+                unsigned long long c[4];
+                part_trav_counters(Ps[i]->trav, c);
+                for (int k = 0; k < 4; ++k) tot[k] += c[k];
+            }
+            have_ctr = true;
+        };
         if (d == HBFS_TOP_DOWN) {
             for (int i = 0; i < nparts; ++i)
                 HB_CHECK(td_owner_counts(Ps[i], world, wper, Ps[i]->counts_dev.as<int64_t>(), st));
@@ -1003,6 +1021,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                             cudaMemcpyDeviceToHost, st));
             }
             HB_CUDA(cudaStreamSynchronize(st));
+            add_trav_counters();
             if (!M)  // recv[i][s] = send[s][i]
                 for (int i = 0; i < nparts; ++i)
                     for (int sr = 0; sr < world; ++sr) hc[(size_t)2 * world * i + world + sr] = hc[(size_t)2 * world * sr + i];
@@ -1062,11 +1081,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                                                P->parent.as<uint32_t>(), P->level.as<int32_t>(),
                                                                part_trav_plane(P->trav, layer + 1),
                                                                P->acnt.as<unsigned long long>());
-                unsigned long long ac[2];
-                HB_CUDA(cudaMemcpyAsync(ac, P->acnt.p, 16, cudaMemcpyDeviceToHost, st));
-                HB_CUDA(cudaStreamSynchronize(st));
-                tot[0] += ac[0];
-                tot[1] += ac[1];
+                HB_CUDA(cudaMemcpyAsync(P->h_acnt, P->acnt.p, 16, cudaMemcpyDeviceToHost, st));
             }
         }
         // next frontier: every rank's owned words of plane layer+1 to everyone
@@ -1081,10 +1096,14 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                                 part_trav_plane(Ps[sr]->trav, layer + 1) + sr * wper, wper * 4,
                                                 cudaMemcpyDeviceToDevice, st));
         }
-        for (int i = 0; i < nparts; ++i)
-            kp_vis_absorb<<<pgrid(nw_pad), 256, 0, st>>>(nw_pad, part_trav_plane(Ps[i]->trav, layer + 1),
-                                                        part_trav_plane(Ps[i]->trav, -1));
-        HB_CUDA(cudaGetLastError());
+        // (the next launch ORs the all-gathered plane into the visited bitmap)
+        HB_CUDA(cudaStreamSynchronize(st));
+        add_trav_counters();
+        if (d == HBFS_TOP_DOWN)
+            for (int i = 0; i < nparts; ++i) {
+                tot[0] += Ps[i]->h_acnt[0];
+                tot[1] += Ps[i]->h_acnt[1];
+            }
         if (M) {
             unsigned long long *ctr = M->ctr.as<unsigned long long>();
             HB_CUDA(cudaMemcpyAsync(ctr, tot, 32, cudaMemcpyHostToDevice, st));
@@ -1103,7 +1122,9 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
             r.g_value = gv;
             r.fallback_count = !p->use_simd || d == HBFS_TOP_DOWN ? 0 : (int64_t)tot[3];
             r.gather_count = !p->use_simd ? 0 : d == HBFS_TOP_DOWN ? e_f : (int64_t)tot[2];
-            r.elapsed = 0.0;
+            const auto now = std::chrono::steady_clock::now();
+            r.elapsed = std::chrono::duration<double>(now - t_layer).count();  // host wall of the layer
+            t_layer = now;
         }
         prev_vf = v_f;
         v_f = (int64_t)tot[0];

@@ -43,6 +43,8 @@ ts = []
 for s in roots:
     res = lb.bfs(s, p)
     ts.append(res.seconds)
+    print(f"  root {s}: {res.seconds * 1e3:.3f} ms summed over ranks: " + " ".join(
+        f"{'B' if x.direction == 'bottom-up' else 'T'}{x.v_f}:{x.elapsed * 1e3:.2f}" for x in res.trace), flush=True)
     outs = lb.outputs()
     lev = np.concatenate([o[1] for o in outs])
     par = np.concatenate([o[0] for o in outs])
