@@ -273,3 +273,23 @@ def test_run_benchmark_csr_cache(cuda, tmp_path):
     assert path.stat().st_mtime_ns == stamp  # reused, not rewritten
     assert [x.source for x in r1.runs] == [x.source for x in r2.runs]
     assert all(x.valid for x in r1.runs + r2.runs)
+
+
+@pytest.mark.parametrize("name", ["k10", "u12", "k11e4"])
+def test_byte_accounting_matches_model(cuda, small_golden, name):
+    """The roofline numerator (hbfs_traversal_bytes) equals the
+    numpy restatement in oracle/bytes_model.py for every direction mix."""
+    hb = cuda
+    from oracle.bytes_model import traversal_bytes as model
+
+    rs, adj = small_golden[f"{name}/rs"], small_golden[f"{name}/adj"]
+    g = hb.from_csr(rs, adj)
+    for s in small_golden[f"{name}/sources"][:3]:
+        s = int(s)
+        for kw in (dict(), dict(force_direction="top-down"), dict(force_direction="bottom-up")):
+            for p in (hb.HeuristicParams(), hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer",
+                                                                   counter_mode="edge")):
+                r = hb.bfs(g, s, p, device=True, **kw)
+                dirs = [1 if x.direction == "bottom-up" else 0 for x in r.trace]
+                want = model(rs, adj, r.level.cpu().numpy(), dirs, rs_bytes=8 if g.wide_offsets else 4)
+                assert hb.traversal_bytes(g, s, r.level, r.trace) == want, (name, s, kw, p.heuristic)

@@ -124,3 +124,24 @@ def test_validator_restatement_faults(oracle):
     b2 = par.copy()
     b2[3] = 0
     assert oracle.validate_tree(g, 0, b2) == (2, 3)
+
+
+def test_byte_model_by_hand():
+    """oracle/bytes_model.py on a path 0-1-2 (4-byte row starts), root 0,
+    layers TD then BU, against a hand count of SURVEY §8(d)."""
+    from oracle.bytes_model import traversal_bytes
+
+    rs = np.array([0, 1, 3, 4])
+    adj = np.array([1, 0, 2, 1], dtype=np.uint32)
+    level = np.array([0, 1, 2])
+    bs, bu = traversal_bytes(rs, adj, level, [0, 1])
+    n, W = 3, 1
+    init = 8 * n + 12 * W
+    # L0 top-down: F={0}: queue 32, rs sector 0, adj sector 0, bitmap sector 0,
+    # parent+level sectors of N={1}: 2*32, next queue 32
+    td = 32 + 32 + 32 + 32 + 64 + 32
+    # L1 bottom-up: U={2} (deg 1, found at position 1 of row [1]... its only
+    # entry), rs sector 0, adj sector 0, bitmap sector 0, parent+level 64
+    bu_l = 4 * W + 32 + 32 + 32 + 64 + 4 * W
+    assert bs == init + td + bu_l
+    assert bu == init + (20 * 1 + 4 * 1 + 12 * 1) + (8 * W + 8 * 1 + 4 * 1 + 8 * 1)
