@@ -931,7 +931,8 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
     for (int i = 0; i < nparts; ++i) {
         Part *P = Ps[i];
         const int rank = M ? M->rank : i;
-        if (P->n != n || P->lo != rank * wper * 32) return set_error(HBFS_EINVAL, "partition does not match rank/world");
+        if (P->n != n || P->lo != std::min<int64_t>(rank * wper * 32, n))
+            return set_error(HBFS_EINVAL, "partition does not match rank/world");
         if (!P->trav) {
             int rc = HBFS_OK;
             P->trav = part_trav_create(n, P->lo, P->nloc, P->arcs, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
