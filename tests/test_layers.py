@@ -203,3 +203,37 @@ def test_cuda_layer_known_answers(cuda):
     # dtype contract of the Cython buffers
     with pytest.raises(ValueError):
         native.bottom_up_layer(rs.astype(np.int32), adj, inw, vis, out, par, 21)
+
+
+def test_native_argument_checks_on_cpu():
+    """Buffer-length and dtype contract of the _native surface (checked before
+    any device work, so it holds on the CPU too)."""
+    from paper_1704_02259_b200 import native
+
+    rs, adj, inw, vis, out, par, n = state(*CASES[0])
+    with pytest.raises(ValueError):
+        native.top_down_layer(rs[:-1], adj, inw, vis, out, par, n)  # rs shorter than n + 1
+    with pytest.raises(ValueError):
+        native.bottom_up_layer(rs, adj, inw[:0], vis, out, par, n)  # frontier bitmap too short
+    with pytest.raises(ValueError):
+        native.top_down_chunked(rs, adj, inw, vis, out, par[:-1], n)  # parent too short
+    with pytest.raises(ValueError):
+        native.bottom_up_layer(rs, adj[:-1], inw, vis, out, par, n)  # adjacency shorter than rs[n]
+    with pytest.raises(ValueError):
+        native.bottom_up_multiple_set(rs, adj, inw, vis, out, par, n, 0, None, vis, vis)  # max_pos < 1
+    with pytest.raises(ValueError):
+        native.bfs_reference(rs, adj[:-1], n, 0)
+
+
+def test_engine_bfs_reference_range_check_on_cpu():
+    from paper_1704_02259_b200 import engine
+
+    class G:  # the attributes engine.bfs_reference reads before any device work
+        num_vertices = 4
+        row_starts = np.zeros(5, dtype=np.int64)
+        adjacency = np.zeros(0, dtype=np.uint32)
+
+    with pytest.raises(IndexError):
+        engine.bfs_reference(G(), 4)
+    with pytest.raises(RuntimeError):
+        engine.bfs_reference(G(), 0, engine="native")  # the reference's CPU engine name
