@@ -1061,11 +1061,25 @@ __device__ __forceinline__ unsigned long long word_append(const Args<OffT> &A, c
 // degree sum of the vertices of word w in `bits`
 template <typename OffT>
 __device__ __forceinline__ uint64_t word_degsum(const Args<OffT> &A, int64_t w, uint32_t bits) {
+    // four vertices per step with their row-start loads issued together
     uint64_t d = 0;
     while (bits) {
-        const uint32_t v = (uint32_t)(w * 32 + __ffs(bits) - 1);
-        bits &= bits - 1;
-        d += (uint64_t)(__ldg(A.rs + v + 1) - __ldg(A.rs + v));
+        uint32_t v[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            ok[j] = bits != 0;
+            v[j] = ok[j] ? (uint32_t)(w * 32 + __ffs(bits) - 1) : 0u;
+            bits &= bits - 1;
+        }
+        OffT a[4], b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a[j] = ok[j] ? __ldg(A.rs + v[j]) : (OffT)0;
+            b[j] = ok[j] ? __ldg(A.rs + v[j] + 1) : (OffT)0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d += (uint64_t)(b[j] - a[j]);
     }
     return d;
 }
