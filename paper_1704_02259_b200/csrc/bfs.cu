@@ -1134,13 +1134,24 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
     const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw;
-    for (int64_t w = wa + tid; w < wb; w += nth) {
-        const uint32_t bits = __ldcg(&out[w]);  // set by the expansion's reductions
-        if (bits) {
-            vis[w] |= bits;
-            acc += ((unsigned long long)__popc(bits) << kPackShift) + word_degsum(A, w, bits);
+    // four words per thread per step: their loads (and the vis words') in flight together
+    for (int64_t w0 = wa + tid; w0 < wb; w0 += 4 * nth) {
+        uint32_t bits[4], vw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t w = w0 + j * nth;
+            bits[j] = w < wb ? __ldcg(&out[w]) : 0u;  // set by the expansion's reductions
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vw[j] = bits[j] ? vis[w0 + j * nth] : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!bits[j]) continue;
+            const int64_t w = w0 + j * nth;
+            vis[w] = vw[j] | bits[j];
+            acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
             if (A.direct_levels)
-                for (uint32_t x = bits; x; x &= x - 1) A.level[w * 32 + __ffs(x) - 1] = depth1;
+                for (uint32_t x = bits[j]; x; x &= x - 1) A.level[w * 32 + __ffs(x) - 1] = depth1;
         }
     }
     acc = warp_sum(acc);
