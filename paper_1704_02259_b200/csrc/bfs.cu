@@ -1185,6 +1185,14 @@ __device__ __forceinline__ int32_t level_of(uint32_t R, const uint32_t (&D)[5], 
     return ((R >> b) & 1u) ? (int32_t)(d0 + rel) : (((vw >> b) & 1u) ? -2 : -1);
 }
 
+// byte I of x as a sign-extended int32 (prmt with the replicate-sign selector)
+template <int I>
+__device__ __forceinline__ int32_t sext_byte(uint32_t x) {
+    int32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "n"(I | (8 | I) << 4 | (8 | I) << 8 | (8 | I) << 12));
+    return r;
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
     const Ctl *c = A.ctl;
@@ -1193,46 +1201,89 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
     if (blockIdx.x == 0 && threadIdx.x == 0) kstamp[3] = globaltimer();
     const int64_t nL = __ldcg(&c->layer);
     const int lane = threadIdx.x & 31;
-    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // tile
     const int64_t d0 = nL + 2 - kPlanes > 0 ? nL + 2 - kPlanes : 0;
-    const int64_t w = t * 32 + lane;
-    if (t * 32 < A.nw) {
-        // lane per word: fold its depth-plane words into binary digit words
-        // (bit b of D_k = bit k of the depth of vertex b relative to d0)
-        const uint32_t vw = w < A.nw ? __ldcs(A.bits + w) : 0u;
-        uint32_t R = 0, D[5] = {0, 0, 0, 0, 0};
-        for (int64_t g0 = d0; g0 < nL; g0 += kLvBatch) {
-            uint32_t p[kLvBatch];
+    const int64_t ntiles = (A.nw + 31) / 32;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool aligned = (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
+    // lane per word: fold its depth-plane words into binary digit words
+    // (bit b of D_k = bit k of the depth of vertex b relative to d0), then the
+    // warp writes its tile's 32 words of levels as full 128-byte lines.  Warps
+    // walk tiles with a stride and load the next tile's planes before storing
+    // the current one (the pass is otherwise a chain of load -> store waves).
+    const bool one_batch = nL - d0 <= kLvBatch;
+    // next tile's plane rows (and its visited row) stream into shared memory
+    // with cp.async while the current tile is folded and stored
+    __shared__ uint32_t stage[kLvBlock / 32][2][kLvBatch + 1][32];
+    uint32_t(*st)[kLvBatch + 1][32] = stage[threadIdx.x >> 5];
+    const int nrow = (int)(nL - d0) + 1;  // planes d0..nL-1, then the visited row
+    auto load_tile = [&](int64_t t, int s) {
+        const int64_t w = t * 32 + lane;
+        const unsigned sz = t < ntiles && w < A.nw ? 4u : 0u;  // zero-fill past the end
+        const int64_t wc = sz ? w : 0;
+        for (int j = 0; j < nrow; ++j) {
+            const uint32_t *src = j + 1 < nrow ? depth_plane(A, d0 + j).p + wc : A.bits + wc;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(&st[s][j][lane]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int s = 0;
+    if (one_batch) load_tile(warp, 0);
+    for (int64_t t = warp; t < ntiles; t += nwarps, s ^= 1) {
+        const int64_t w = t * 32 + lane;
+        uint32_t R = 0, D[5] = {0, 0, 0, 0, 0}, vw;
+        if (one_batch) {
+            load_tile(t + nwarps, s ^ 1);  // in flight while this tile is stored
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            __syncwarp();
+            for (int j = 0; j + 1 < nrow; ++j) {
+                const uint32_t p = st[s][j][lane];
+                R |= p;
 #pragma unroll
-            for (int j = 0; j < kLvBatch; ++j)
-                p[j] = w < A.nw && g0 + j < nL ? __ldcs(depth_plane(A, g0 + j).p + w) : 0u;
+                for (int k = 0; k < 5; ++k) D[k] |= ((j >> k) & 1) ? p : 0u;
+            }
+            vw = st[s][nrow - 1][lane];
+            __syncwarp();  // stage s is refilled next iteration
+        } else {  // deep traversals: all held planes, batch by batch
+            vw = w < A.nw ? __ldcs(A.bits + w) : 0u;
+            for (int64_t g0 = d0; g0 < nL; g0 += kLvBatch) {
+                uint32_t p[kLvBatch];
 #pragma unroll
-            for (int j = 0; j < kLvBatch; ++j) {
-                const uint32_t rel = (uint32_t)(g0 + j - d0);
-                R |= p[j];
+                for (int j = 0; j < kLvBatch; ++j)
+                    p[j] = w < A.nw && g0 + j < nL ? __ldcs(depth_plane(A, g0 + j).p + w) : 0u;
 #pragma unroll
-                for (int k = 0; k < 5; ++k) D[k] |= ((rel >> k) & 1u) ? p[j] : 0u;
+                for (int j = 0; j < kLvBatch; ++j) {
+                    const uint32_t rel = (uint32_t)(g0 + j - d0);
+                    R |= p[j];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) D[k] |= ((rel >> k) & 1u) ? p[j] : 0u;
+                }
             }
         }
-        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n &&  // warp-uniform
-                          (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
+        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n && aligned;  // warp-uniform
         if (fast) {
             // round r: the warp writes words 4r..4r+3 of the tile (512
             // contiguous bytes, four full lines); lane l takes levels
-            // 4(l%8)..+3 of word 4r + l/8
-            const int q = lane & 7;
+            // 4(l%8)..+3 of word 4r + l/8.  Nothing is flushed (d0 = 0), so
+            // visited implies reached and a level is its 5 digit bits: the
+            // four vertices' digit nibbles are spread one bit per byte
+            // (x * 0x00204081 puts bit i at byte i), unreached bytes become
+            // 0xFF, and a sign-extending byte permute widens each to int32.
+            const int b0 = 4 * (lane & 7);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int src = 4 * r + (lane >> 3);
-                const uint32_t Rs = __shfl_sync(0xffffffffu, R, src);
-                const uint32_t vs = __shfl_sync(0xffffffffu, vw, src);
-                uint32_t Ds[5];
+                uint32_t v = 0;
 #pragma unroll
-                for (int k = 0; k < 5; ++k) Ds[k] = __shfl_sync(0xffffffffu, D[k], src);
+                for (int k = 0; k < 5; ++k) {
+                    const uint32_t nib = (__shfl_sync(0xffffffffu, D[k], src) >> b0) & 0xFu;
+                    v |= (nib * (0x00204081u << k)) & (0x01010101u << k);
+                }
+                const uint32_t hit = (((__shfl_sync(0xffffffffu, R, src) >> b0) & 0xFu) * 0x00204081u) & 0x01010101u;
+                v |= (hit ^ 0x01010101u) * 0xFFu;
                 int4 *gdst = reinterpret_cast<int4 *>(A.level + (t * 32 + src) * 32);
-                const int b0 = 4 * q;
-                __stcs(gdst + q, make_int4(level_of(Rs, Ds, vs, d0, b0), level_of(Rs, Ds, vs, d0, b0 + 1),
-                                           level_of(Rs, Ds, vs, d0, b0 + 2), level_of(Rs, Ds, vs, d0, b0 + 3)));
+                __stcs(gdst + (lane & 7), make_int4(sext_byte<0>(v), sext_byte<1>(v), sext_byte<2>(v), sext_byte<3>(v)));
             }
         } else if (w < A.nw) {
             int32_t *dst = A.level + w * 32;
@@ -1554,7 +1605,7 @@ struct Workspace {
     DevBuf cbq, cbqo, cbqr, cbcs;  // column-blocked top-down segment queues
     int cb_ranges = 0;
     int64_t ncs = 0;  // chunk-start entries per queue buffer
-    int grid = 0;
+    int grid = 0, lv_grid = 0;
     size_t smem = 0;
     const void *fn = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1623,6 +1674,9 @@ static int ws_alloc(hbfs_graph *g) {
         if (e != cudaSuccess || per_sm < 1)
             rc = set_error(HBFS_ECUDA, "occupancy query failed: %s", cudaGetErrorString(e));
         w->grid = per_sm * sms;
+        int lv_per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lv_per_sm, levels_kernel<OffT>, kLvBlock, 0);
+        w->lv_grid = std::max(1, lv_per_sm) * sms * (int)env_i64("HBFS_LV_WAVES", 1);
     }
     if (rc) {
         delete w;
@@ -1700,7 +1754,8 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         if (!A.direct_levels) {  // no-op unless this launch finished the traversal
             const int64_t tiles = (g->nw + 31) / 32;
             const int64_t per = kLvBlock / 32;
-            levels_kernel<OffT><<<(unsigned)((tiles + per - 1) / per), kLvBlock, 0, st>>>(A);
+            const int64_t blocks = std::min<int64_t>((tiles + per - 1) / per, (int64_t)w->lv_grid);
+            levels_kernel<OffT><<<(unsigned)std::max<int64_t>(1, blocks), kLvBlock, 0, st>>>(A);
             HB_CUDA(cudaGetLastError());
         }
         HB_CUDA(cudaEventRecord(w->ev1, st));
