@@ -111,6 +111,23 @@ def test_deep_path_resumes_across_launches(cuda, oracle, monkeypatch, defer):
     assert [t.direction == "bottom-up" for t in r.trace] == [bool(x["direction"]) for x in rows]
 
 
+@pytest.mark.parametrize("depth", [10, 25, 40])
+def test_deferred_levels_full_tiles(cuda, oracle, monkeypatch, depth):
+    """levels_kernel paths on full 1024-vertex tiles: all planes in one staged
+    batch (depth <= 16), several batches with nothing flushed (16 < depth <
+    31), and flushed planes (depth > 30: the per-bit path keeps the levels
+    written when a plane was recycled); unreached vertices stay -1."""
+    monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
+    n = 6000
+    rng = np.random.default_rng(depth)
+    spine = list(range(depth + 1))
+    pairs = [(spine[i], spine[i + 1]) for i in range(depth)]
+    # every other vertex below 5000 hangs off a random spine vertex; 5000.. unreached
+    pairs += [(int(rng.integers(0, depth + 1)), v) for v in range(depth + 1, 5000)]
+    pairs += [(v, v + 1) for v in range(5000, n - 1, 2)]
+    check_all(cuda, oracle, pairs, n, roots=[0, depth // 2, 4000])
+
+
 def test_errors(cuda):
     hb = cuda
     g, _, _ = graph(hb, [(0, 1), (1, 2)], 3)
