@@ -535,17 +535,34 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
 
 // ---------------------------------------------------------------- phases
 
+// a[i] = (i == special ? sv : x) for i in [i0, i1): 16-byte stores over the
+// aligned body, scalar head and tail (the buffers may be caller views)
+__device__ __forceinline__ void fill_words(uint32_t *a, int64_t i0, int64_t i1, uint32_t x,
+                                           int64_t special, uint32_t sv, int64_t tid, int64_t nth) {
+    if (i1 <= i0) return;
+    int64_t b0 = i0 + (int64_t)((16 - (reinterpret_cast<uintptr_t>(a + i0) & 15)) & 15) / 4;
+    if (b0 > i1) b0 = i1;
+    const int64_t nv = (i1 - b0) / 4, b1 = b0 + nv * 4;
+    for (int64_t i = i0 + tid; i < b0; i += nth) a[i] = i == special ? sv : x;
+    for (int64_t i = b1 + tid; i < i1; i += nth) a[i] = i == special ? sv : x;
+    uint4 *av = reinterpret_cast<uint4 *>(a + b0);
+    for (int64_t q = tid; q < nv; q += nth) {
+        uint4 y = make_uint4(x, x, x, x);
+        const int64_t r = special - (b0 + 4 * q);
+        if ((uint64_t)r < 4) (r == 0 ? y.x : r == 1 ? y.y : r == 2 ? y.z : y.w) = sv;
+        av[q] = y;
+    }
+}
+
 template <typename OffT, bool PART = false>
 __device__ void phase_init(const Args<OffT> &A) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const uint32_t root = A.root;
     const int64_t v0 = PART ? A.part_lo : 0, v1 = PART ? A.part_lo + A.part_nown : A.n;
-    for (int64_t i = v0 + tid; i < v1; i += nth) {
-        const bool r = i == (int64_t)root;
-        A.parent[i] = r ? root : HBFS_NIL;
-        if (A.direct_levels) A.level[i] = r ? 0 : -1;
-    }
+    fill_words(A.parent, v0, v1, HBFS_NIL, (int64_t)root, root, tid, nth);
+    if (A.direct_levels)
+        fill_words(reinterpret_cast<uint32_t *>(A.level), v0, v1, 0xFFFFFFFFu, (int64_t)root, 0u, tid, nth);
     // vis and B0 hold the root; B1, B2 zero
     const int64_t rw = root >> 5;
     const uint32_t rb = 1u << (root & 31);
