@@ -11,8 +11,9 @@ outside the events.  value = harmonic mean of m / t over all timed traversals
 
 Extra keys:
   e2e          same metric through the reference-facing call with HOST outputs
-               (hybrid_bfs-style: kernel + D2H of parent and level into pinned
-               host memory, wall clock per traversal)
+               (hybrid_bfs(g, root, out=...) -> (BfsTree, trace): kernel + trace
+               + D2H of the parent array into pinned host memory, wall clock
+               per traversal)
   roofline     B_sector (SURVEY §8(d) byte model, device accounting pass) per
                traversal / kernel time vs MEASURED_PEAKS.json hbm_gbs
   cpu_baseline the reference's compiled CPU kernels (oracle/_ref) on a bounded
@@ -367,16 +368,20 @@ def run_ours(args, cfg):
     traffic = profiled_traffic(cfg["label"])
     rnd = random_sector_ceiling()
 
-    # --- e2e: reference-facing call with host outputs (kernel + D2H into pinned memory)
-    hpar = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    hlev = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+    # --- e2e: the reference-facing call, hybrid_bfs(g, s) -> (BfsTree, trace), exactly as
+    # a user makes it (kernel + trace + D2H of the parent array into the host result,
+    # which hybrid_bfs takes from the pinned caching allocator)
     e2e_secs = []
+    hb.hybrid_bfs(g, int(roots[0]), p, use_simd=True, engine_name="cuda",
+                  parent_mode=args.parent_mode)  # warm-up: fills the pinned-block cache
     for s in roots:
         flush.fill_(1)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        hb.bfs(g, int(s), p, use_simd=True, parent_mode=args.parent_mode, device=False,
-               trace=True, out=(hpar, hlev))
+        tree, _ = hb.hybrid_bfs(g, int(s), p, use_simd=True, engine_name="cuda",
+                                parent_mode=args.parent_mode)
+        assert tree.parent[int(s)] == int(s)
+        del tree
         e2e_secs.append(time.perf_counter() - t1)
     e2e_value = len(e2e_secs) * m / sum(e2e_secs) / 1e9
 
@@ -407,7 +412,8 @@ def run_ours(args, cfg):
                                            "and uniformly random; the attainable ceiling for data-dependent "
                                            "sector traffic, next to the copy-bandwidth peak"},
         "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 4 * len(roots),
-                "d2h_bytes_per_step": len(roots) * (8 * n + 256)},
+                "d2h_bytes_per_step": len(roots) * (4 * n + 256),
+                "call": "hybrid_bfs(g, root) per root: BfsTree parents (host) + trace"},
         "clocks": clk.summary(),
     }
     if ws == 1 and not args.no_cpu_baseline:

@@ -1771,7 +1771,9 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         void *kargs[] = {&A};
         HB_CUDA(cudaLaunchCooperativeKernel(w->fn, dim3(w->grid),
                                             dim3(kBlock), kargs, w->smem, st));
-        if (!A.direct_levels) {  // no-op unless this launch finished the traversal
+        // no-op unless this launch finished the traversal; skipped when the
+        // caller asked for parents only (hybrid_bfs: the reference's BfsTree)
+        if (!A.direct_levels && level) {
             const int64_t tiles = (g->nw + 31) / 32;
             const int64_t per = kLvBlock / 32;
             const int64_t blocks = std::min<int64_t>((tiles + per - 1) / per, (int64_t)w->lv_grid);

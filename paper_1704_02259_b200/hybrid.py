@@ -113,6 +113,19 @@ class BfsResult:
 
 
 _TRACE_CAP = 4096
+_PINNED_MIN_N = 1 << 16
+
+
+def _host_parent(n: int) -> np.ndarray:
+    """Result array for hybrid_bfs.  Large outputs come from torch's caching
+    pinned-host allocator, so the device-to-host copy runs at full PCIe rate
+    (pageable memory takes a driver staging copy); the block returns to the
+    cache when the caller drops the array (the ndarray holds the tensor)."""
+    if n >= _PINNED_MIN_N:
+        import torch
+
+        return torch.empty(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    return np.empty(n, dtype=np.uint32)
 
 
 def _run(g, source: int, hp: _lib.hbfs_params, parent, level, on_device: bool, want_trace: bool,
@@ -148,8 +161,11 @@ def _run(g, source: int, hp: _lib.hbfs_params, parent, level, on_device: bool, w
 
 def hybrid_bfs(g, source: int, p: HeuristicParams | None = None, cfg: VecConfig | None = None,
                use_simd: bool = False, engine_name: str = "auto",
-               force_direction: str | None = None, parent_mode: str = "minid"):
-    """Full traversal (hybrid.py:83-175) → (BfsTree, trace)."""
+               force_direction: str | None = None, parent_mode: str = "minid", out=None):
+    """Full traversal (hybrid.py:83-175) → (BfsTree, trace).
+
+    Parents only, as the reference's ``BfsTree`` (frontier.py:95-107); no level
+    array is produced.  ``out`` reuses a host uint32[n] buffer (e.g. pinned)."""
     p = p if p is not None else HeuristicParams()
     cfg = cfg if cfg is not None else VecConfig()
     engine.resolve_engine(engine_name, cfg.backend)
@@ -158,7 +174,12 @@ def hybrid_bfs(g, source: int, p: HeuristicParams | None = None, cfg: VecConfig 
     if not 0 <= source < n:
         raise IndexError(f"source {source} out of range [0, {n})")
     hp = _params(p, cfg, use_simd, force_direction, parent_mode)
-    parent = np.empty(n, dtype=np.uint32)
+    if out is None:
+        parent = _host_parent(n)
+    else:
+        parent = out
+        if parent.dtype != np.uint32 or parent.shape != (n,) or not parent.flags.c_contiguous:
+            raise ValueError("out must be a contiguous uint32 array of length n")
     trace, _ = _run(dg, int(source), hp, parent.ctypes.data_as(C.c_void_p), None, False, True,
                     use_simd)
     return BfsTree(parent=parent, source=int(source)), trace

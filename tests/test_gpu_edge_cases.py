@@ -128,6 +128,32 @@ def test_deferred_levels_full_tiles(cuda, oracle, monkeypatch, depth):
     check_all(cuda, oracle, pairs, n, roots=[0, depth // 2, 4000])
 
 
+@pytest.mark.parametrize("defer", [False, True])
+def test_hybrid_bfs_parents_only_out_buffer(cuda, oracle, monkeypatch, defer):
+    """hybrid_bfs returns parents only (no level stamping pass) into a reused
+    host buffer; a following bfs() on the same workspace still stamps levels."""
+    if defer:
+        monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
+    hb = cuda
+    n = 5000
+    rng = np.random.default_rng(7)
+    pairs = [(int(a), int(b)) for a, b in rng.integers(0, n, size=(20000, 2))]
+    g, eu, ev = graph(hb, pairs, n)
+    host = oracle.csr_build(eu, ev, n)
+    buf = np.empty(n, dtype=np.uint32)
+    for s in (0, 17, 4999):
+        par, lev, rows = oracle.hybrid_bfs(host, s, use_simd=True)
+        tree, trace = hb.hybrid_bfs(g, s, use_simd=True, out=buf)
+        assert tree.parent is buf and np.array_equal(buf, par)
+        assert len(trace) == len(rows)
+        r = hb.bfs(g, s, use_simd=True, device=False)
+        assert np.array_equal(r.level, lev) and np.array_equal(r.parent, par)
+    with pytest.raises(ValueError):
+        hb.hybrid_bfs(g, 0, out=np.empty(n, dtype=np.int64))
+    with pytest.raises(ValueError):
+        hb.hybrid_bfs(g, 0, out=np.empty(n - 1, dtype=np.uint32))
+
+
 def test_errors(cuda):
     hb = cuda
     g, _, _ = graph(hb, [(0, 1), (1, 2)], 3)
