@@ -19,6 +19,7 @@ Parents are identical in every mode (min-id rule) with
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -120,8 +121,10 @@ def _host_parent(n: int) -> np.ndarray:
     """Result array for hybrid_bfs.  Large outputs come from torch's caching
     pinned-host allocator, so the device-to-host copy runs at full PCIe rate
     (pageable memory takes a driver staging copy); the block returns to the
-    cache when the caller drops the array (the ndarray holds the tensor)."""
-    if n >= _PINNED_MIN_N:
+    cache when the caller drops the array (the ndarray holds the tensor).
+    Cached pinned blocks stay page-locked until the process exits; callers that
+    keep many trees alive can set HBFS_PINNED_RESULTS=0 for pageable arrays."""
+    if n >= _PINNED_MIN_N and os.environ.get("HBFS_PINNED_RESULTS", "1") != "0":
         import torch
 
         return torch.empty(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)

@@ -128,3 +128,13 @@ def test_csr_cache_roundtrip(tmp_path, oracle):
     (tmp_path / "bad.csr").write_bytes(bytes(raw))
     with pytest.raises(ValueError):
         csr.load_arrays(tmp_path / "bad.csr")
+
+
+def test_host_parent_result_arrays(monkeypatch):
+    # small results (and HBFS_PINNED_RESULTS=0) are plain pageable uint32 arrays;
+    # large ones come from the pinned caching allocator (needs CUDA: GPU tests)
+    a = hybrid._host_parent(100)
+    assert a.dtype == np.uint32 and a.shape == (100,) and a.flags.c_contiguous
+    monkeypatch.setenv("HBFS_PINNED_RESULTS", "0")
+    b = hybrid._host_parent(1 << 20)
+    assert b.dtype == np.uint32 and b.shape == (1 << 20,) and b.base is None
