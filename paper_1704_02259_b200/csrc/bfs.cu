@@ -1765,8 +1765,17 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     const Ctl *hc = static_cast<const Ctl *>(w->h_ctl);
     const hbfs_layer_row *hrows =
         reinterpret_cast<const hbfs_layer_row *>(static_cast<const char *>(w->h_ctl) + sizeof(Ctl));
+    auto copy_out = [&]() -> int {
+        if (parent)
+            HB_CUDA(cudaMemcpyAsync(parent, A.parent, g->n * 4, cudaMemcpyDeviceToHost, st));
+        if (level)
+            HB_CUDA(cudaMemcpyAsync(level, A.level, g->n * 4, cudaMemcpyDeviceToHost, st));
+        return HBFS_OK;
+    };
+    int launches = 0;
     HB_CUDA(cudaEventRecord(w->ev0, st));
     for (int launch = 0;; ++launch) {
+        ++launches;
         A.do_init = launch == 0;
         void *kargs[] = {&A};
         HB_CUDA(cudaLaunchCooperativeKernel(w->fn, dim3(w->grid),
@@ -1784,6 +1793,13 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         // Ctl plus the first rows in one copy; the rest only if needed.
         const size_t head = sizeof(Ctl) + 64 * sizeof(hbfs_layer_row);
         HB_CUDA(cudaMemcpyAsync(w->h_ctl, A.ctl, head, cudaMemcpyDeviceToHost, st));
+        // host outputs: queue their copies behind the first launch, so a
+        // traversal that finishes in it (all but > kRowsCap layers) costs one
+        // stream synchronisation; a resumed traversal copies again at the end
+        if (!dev_out && launch == 0) {
+            const int rc = copy_out();
+            if (rc) return rc;
+        }
         HB_CUDA(cudaStreamSynchronize(st));
         const int64_t rows = hc->rows;
         if (rows > 64) {
@@ -1799,13 +1815,11 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         if (hc->done) break;  // else: > kRowsCap layers, resume from the persisted state
     }
     if (n_layers) *n_layers = total;
-    if (!dev_out) {
-        if (parent)
-            HB_CUDA(cudaMemcpyAsync(parent, A.parent, g->n * 4, cudaMemcpyDeviceToHost, st));
-        if (level)
-            HB_CUDA(cudaMemcpyAsync(level, A.level, g->n * 4, cudaMemcpyDeviceToHost, st));
+    if (!dev_out && launches > 1) {
+        const int rc = copy_out();
+        if (rc) return rc;
+        HB_CUDA(cudaStreamSynchronize(st));
     }
-    HB_CUDA(cudaStreamSynchronize(st));
     if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, w->ev0, w->ev1));
     return HBFS_OK;
 }

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -114,6 +115,7 @@ class BfsResult:
 
 
 _TRACE_CAP = 4096
+_tls = threading.local()
 _PINNED_MIN_N = 1 << 16
 
 
@@ -137,7 +139,9 @@ def _run(g, source: int, hp: _lib.hbfs_params, parent, level, on_device: bool, w
     n_layers = C.c_int64()
     ms = C.c_float()
     cap = _TRACE_CAP if want_trace else 0
-    rows = (_lib.hbfs_layer_row * max(cap, 1))()
+    rows = getattr(_tls, "rows", None)  # reused per thread: rows are copied out below
+    if rows is None:
+        rows = _tls.rows = (_lib.hbfs_layer_row * _TRACE_CAP)()
     pp = C.c_void_p(parent) if isinstance(parent, int) else parent
     lp = C.c_void_p(level) if isinstance(level, int) else level
     stream = _lib.current_stream() if on_device else None
