@@ -41,7 +41,10 @@ void clear_error();
         return ::hbfs::set_error(HBFS_ECUDA, "internal error");                \
     }
 
-constexpr int kBlock = 512;  // threads per CTA for the traversal kernels
+#ifndef HBFS_KBLOCK
+#define HBFS_KBLOCK 512
+#endif
+constexpr int kBlock = HBFS_KBLOCK;  // threads per CTA for the traversal kernels
 
 struct Workspace;
 

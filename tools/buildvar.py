@@ -21,7 +21,8 @@ def main(bfs_src, out):
             src = src2
         obj = os.path.join(d, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, "-I", os.path.join(B.REPO, "include"), "-I", B.CSRC, "-c", src, "-o", obj]
+        extra = os.environ.get("HBFS_VAR_FLAGS", "").split()  # e.g. -DHBFS_KBLOCK=384
+        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *extra, "-I", os.path.join(B.REPO, "include"), "-I", B.CSRC, "-c", src, "-o", obj]
         procs.append(subprocess.Popen(cmd))
     for p in procs:
         assert p.wait() == 0
