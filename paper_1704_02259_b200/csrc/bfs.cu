@@ -1693,7 +1693,8 @@ static int ws_alloc(hbfs_graph *g) {
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w->fn, kBlock, w->smem);
         if (e != cudaSuccess || per_sm < 1)
             rc = set_error(HBFS_ECUDA, "occupancy query failed: %s", cudaGetErrorString(e));
-        w->grid = (int)std::min<int64_t>(per_sm, env_i64("HBFS_GRID_PER_SM", per_sm)) * sms;
+        w->grid = (int)(std::min<int64_t>(per_sm, env_i64("HBFS_GRID_PER_SM", per_sm)) *
+                        std::min<int64_t>(sms, env_i64("HBFS_GRID_SMS", sms)));
         int lv_per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lv_per_sm, levels_kernel<OffT>, kLvBlock, 0);
         w->lv_grid = std::max(1, lv_per_sm) * sms * (int)env_i64("HBFS_LV_WAVES", 1);
