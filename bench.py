@@ -16,8 +16,9 @@ Extra keys:
                per traversal)
   roofline     B_sector (SURVEY §8(d) byte model, device accounting pass) per
                traversal / kernel time vs MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline the reference's compiled CPU kernels (oracle/_ref) on a bounded
-               sample of roots, timed like harness._run_one
+  cpu_baseline the STOCK reference (oracle/_ref: hybfs.hybrid_bfs on its
+               compiled engine, timed by hybfs.harness._run_one) on a bounded
+               sample of distinct roots, concurrent worker processes
   clocks       nvidia-smi samples taken during the timed region
 
 --impl reference runs the reference's CPU path instead (rank 0 only).
@@ -204,86 +205,90 @@ def profiled_traffic(label):
 
 # --------------------------------------------------------------- reference
 
-def reference_graph(cfg):
-    from oracle import oracle as O
-    from oracle import ref_runner
-
-    O.build()
-    u, v = O.generate(cfg["scale"], 16, 1, cfg["probs"])
-    h = O.csr_build(u, v, 1 << cfg["scale"])
-    del u, v
-    return h, ref_runner.RefGraph(h.row_starts, h.adjacency, h.in_edges_total)
-
-
-def reference_sample_size(cfg):
-    return {16: 64, 20: 16, 22: 4, 26: 1}.get(cfg["scale"], 4)
+def reference_roots_per_step(cfg, workers):
+    """Traversals per reference step: every root on graphs the CPU sweeps in
+    seconds, else one wave of `workers` concurrent roots (at least 8 over the
+    run), rotating through the 64 sampled roots from step to step."""
+    if cfg["scale"] <= 22:
+        return ROOTS
+    return max(workers, 2)
 
 
 def run_reference(args, cfg):
-    from oracle import oracle as O
-    from oracle import ref_runner
+    """The reference's own CPU path (the STOCK hybfs package in oracle/_ref: its
+    hybrid_bfs controller on its compiled native engine, timed by its
+    harness._run_one), on this host's cores: `workers` single-threaded
+    traversals of distinct roots run concurrently (oracle/refbench.py)."""
+    from oracle import refbench
 
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    h, rg = reference_graph(cfg)
-    roots = O.sample_sources(h, ROOTS, 1)
-    k = reference_sample_size(cfg)
-    sample = roots[:k]
-    for _ in range(args.warmup if cfg["scale"] < 24 else 1):
-        ref_runner.time_roots(rg, sample[:1], **cfg["ref"])
-    secs = []
+    g, built = refbench.stock_graph(cfg["scale"], 16, 1, cfg["probs"])
+    roots = refbench.sample_sources(g, ROOTS, 1)
+    workers = refbench.workers_available()
+    k = reference_roots_per_step(cfg, workers)
+    a, b = cfg["ref"]["alpha"], cfg["ref"]["beta"]
+    order = [roots[i % ROOTS] for i in range((args.steps + 1) * k)]
+    refbench.time_roots(g, order[:min(k, workers)], a, b, workers)  # warm-up wave (untimed)
+    crit = 0.0
+    per_root = []
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s, _r = ref_runner.time_roots(rg, sample, **cfg["ref"])
-        secs += s
+    for step in range(args.steps):
+        r = refbench.time_roots(g, order[step * k:(step + 1) * k], a, b, workers)
+        crit += r["critical_s"]
+        per_root += r["per_root"]
     wall = time.perf_counter() - t0
-    m = h.in_edges_total
-    value = len(secs) * m / sum(secs) / 1e9
-    info = ref_runner.cpu_info()
+    m = g.in_edges_total
+    value = len(per_root) * m / crit / 1e9
+    per_trav = len(per_root) * m / sum(x[1] for x in per_root) / 1e9
+    distinct = len({x[0] for x in per_root})
+    info = refbench.cpu_info()
+    sample = (f"{k} roots per step ({distinct} distinct of the 64 sampled roots over the run), "
+              f"{min(workers, k)} concurrent single-threaded stock traversals "
+              f"(hybfs.harness._run_one, simd-hybrid, alpha={a} beta={b}, native engine {info['variant']}); "
+              f"graph: {built}")
     line = {
         "impl": "reference",
         "metric": "harmonic-mean GTEPS over 64 roots",
         "value": value, "unit": "GTEPS", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (reference R-MAT generator restated, seed 1)",
+        "data": "synthetic (reference R-MAT generator, seed 1)",
         "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
-                   "roots_per_step": int(k), "mode": "simd-hybrid", **cfg["ref"]},
-        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
-                         "sample": f"{k} of the 64 sampled roots per step, reference native "
-                                   f"kernels (hybfs._native, {info['variant']}), 1 thread",
-                         **info},
+                   "roots_per_step": int(k), "distinct_roots": distinct, "mode": "simd-hybrid",
+                   "alpha": a, "beta": b},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": min(workers, k), "kind": "reference",
+                         "sample": sample, "per_traversal_gteps": per_trav, **info},
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_for(cfg, g=None):
-    """Bounded reference CPU sample for the N=1 line.  The host CSR is the device
-    graph exported in the reference layout (bit-exact with csr.build, tested), so
-    SCALE 26 does not need a CPU-side generation."""
-    from oracle import oracle as O
-    from oracle import ref_runner
+def cpu_baseline_for(cfg, g):
+    """Bounded reference CPU sample for the N=1 line: the stock hybfs on the
+    device graph exported in the reference layout (byte-identical to the
+    reference arm's graph, tests/golden/hashes_s26.json), one wave of
+    concurrent single-threaded traversals of distinct roots (>= 8)."""
+    from oracle import refbench
 
-    if g is None:
-        h, rg = reference_graph(cfg)
-    else:
-        h = O.HostCsr(g.num_vertices, np.asarray(g.row_starts), np.asarray(g.adjacency),
-                      g.in_edges_total)
-        rg = ref_runner.RefGraph(h.row_starts, h.adjacency, h.in_edges_total)
-    roots = O.sample_sources(h, ROOTS, 1)
-    k = reference_sample_size(cfg)
     t0 = time.perf_counter()
-    secs, _ = ref_runner.time_roots(rg, roots[:k], **cfg["ref"])
-    value = len(secs) * h.in_edges_total / sum(secs) / 1e9
-    info = ref_runner.cpu_info()
-    return {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
-            "sample": f"{k} of the 64 sampled roots, simd-hybrid with the reference rule "
-                      f"alpha={cfg['ref']['alpha']} beta={cfg['ref']['beta']}, reference "
-                      f"native kernels ({info['variant']}), 1 thread (reference is single-threaded)",
-            "seconds": time.perf_counter() - t0, **info}
+    hg = refbench.wrap(g.num_vertices, g.row_starts, g.adjacency, g.in_edges_total)
+    roots = refbench.sample_sources(hg, ROOTS, 1)
+    workers = refbench.workers_available()
+    k = ROOTS if cfg["scale"] <= 22 else max(8, workers)
+    a, b = cfg["ref"]["alpha"], cfg["ref"]["beta"]
+    r = refbench.time_roots(hg, roots[:k], a, b, workers)
+    m = hg.in_edges_total
+    value = len(r["per_root"]) * m / r["critical_s"] / 1e9
+    per_trav = len(r["per_root"]) * m / sum(x[1] for x in r["per_root"]) / 1e9
+    info = refbench.cpu_info()
+    return {"value": value, "unit": "GTEPS", "cores": r["workers"], "kind": "reference",
+            "sample": f"the first {k} of the 64 sampled roots, {r['workers']} concurrent single-threaded "
+                      f"stock traversals (hybfs.harness._run_one, simd-hybrid, reference rule "
+                      f"alpha={a} beta={b}, native engine {info['variant']})",
+            "per_traversal_gteps": per_trav, "seconds": time.perf_counter() - t0, **info}
 
 
 # -------------------------------------------------------------------- ours

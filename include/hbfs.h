@@ -115,7 +115,10 @@ int hbfs_sample_sources(const hbfs_graph *g, int64_t count, uint64_t seed, int a
  * parent: uint32[n] (NIL = unreached), level: int32[n] (-1 = unreached); either
  * may be NULL.  on_device says where parent/level live.  trace: host array of
  * trace_cap rows (may be NULL); *n_layers receives the total layer count.
- * *device_ms receives the device time of init + traversal (CUDA events). */
+ * *device_ms receives the device time of init + traversal (CUDA events).
+ * Thread safety: calls on the same graph are serialised (a per-graph lock is
+ * held for the whole call, which returns after its stream work completed);
+ * different graphs may be traversed concurrently. */
 int hbfs_bfs(hbfs_graph *g, int64_t root, const hbfs_params *p, uint32_t *parent,
              int32_t *level, int on_device, hbfs_layer_row *trace, int64_t trace_cap,
              int64_t *n_layers, float *device_ms, void *stream);
@@ -150,6 +153,11 @@ int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows);
  * buffer, each warp's 32 lanes inside one random 2^log_region-byte region (the
  * access pattern of the traversal's gathers; bench.py's second roofline). */
 int hbfs_probe_random_sectors(int log_bytes, int log_region, double *gbs);
+
+/* Tuning: set the L2 -> DRAM fetch granularity of the current context
+ * (cudaLimitMaxL2FetchGranularity, bytes <= 128; bytes < 0 only queries);
+ * *previous (may be NULL) receives the old value. */
+int hbfs_l2_fetch_granularity(int bytes, int *previous);
 
 /* ---- per-layer steps on caller buffers: the hybfs._native surface ----
  * All pointers are DEVICE pointers in the reference's layout: rs int64[n+1],

@@ -49,11 +49,34 @@ def built_paths() -> dict:
     }
 
 
+def install_package(quiet: bool = True) -> None:
+    """Ship the reference's stock Python package next to each compiled _native:
+    the unmodified ``hybfs/*.py`` of /root/reference land in
+    ``oracle/_ref/<variant>/hybfs/`` (git-ignored build output, like the .so),
+    so the GPU box can import the stock ``hybfs`` — its controller
+    (``hybrid.hybrid_bfs``), engine dispatch and harness — for the bench's
+    reference arm and the reference-side integration tests
+    (``oracle.refpkg``).  Files are copied verbatim and never edited."""
+    for variant in VARIANTS:
+        dst = os.path.join(OUT_ROOT, variant, "hybfs")
+        os.makedirs(dst, exist_ok=True)
+        for name in sorted(os.listdir(REF_SRC)):
+            if not name.endswith(".py"):
+                continue
+            src = os.path.join(REF_SRC, name)
+            out = os.path.join(dst, name)
+            if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+                shutil.copyfile(src, out)
+        if not quiet:
+            print(f"stock hybfs package ({variant}) -> {dst}")
+
+
 def build(force: bool = False, quiet: bool = True) -> dict:
     """Build both variants if the reference sources are present; return paths."""
     paths = built_paths()
     if not os.path.isdir(REF_SRC):
         return {v: p for v, p in paths.items() if os.path.exists(p)}
+    install_package(quiet)
     pyx = os.path.join(REF_SRC, "_native.pyx")
     hdr = os.path.join(REF_SRC, "bu_probe.h")
     src_mtime = max(os.path.getmtime(pyx), os.path.getmtime(hdr))

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import weakref
 
 import numpy as np
 
@@ -151,15 +152,34 @@ def as_device_graph(g) -> CsrGraph:
     """Accept our CsrGraph or any object with the reference CsrGraph fields."""
     if isinstance(g, CsrGraph):
         return g
-    cache = _IMPORTED.get(id(g))
-    if cache is not None and cache[0] is g:
+    key = id(g)
+    cache = _IMPORTED.get(key)
+    if cache is not None and cache[0]() is g:
         return cache[1]
     dg = from_csr(g.row_starts, g.adjacency, getattr(g, "in_edges_total", None))
-    _IMPORTED[id(g)] = (g, dg)
+    try:
+        ref = weakref.ref(g)
+        # the device copy (and its workspace) is freed with the host graph
+        weakref.finalize(g, _drop_imported, key, dg)
+    except TypeError:  # not weak-referenceable: keep only the latest import
+        for k in [k for k, v in _IMPORTED.items() if v[2]]:
+            _drop_imported(k, _IMPORTED[k][1])
+        ref = (lambda obj: (lambda: obj))(g)
+        _IMPORTED[key] = (ref, dg, True)
+        return dg
+    _IMPORTED[key] = (ref, dg, False)
     return dg
 
 
+# id(host graph) -> (weak reference, device CsrGraph, strongly held?)
 _IMPORTED: dict = {}
+
+
+def _drop_imported(key, dg) -> None:
+    cur = _IMPORTED.get(key)
+    if cur is not None and cur[1] is dg:
+        del _IMPORTED[key]
+    dg.free()
 
 
 def degree(g: CsrGraph, v: int) -> int:

@@ -2001,6 +2001,7 @@ extern "C" int hbfs_bfs(hbfs_graph *g, int64_t root, const hbfs_params *p, uint3
     if (g->n >= (int64_t(1) << 29))
         return set_error(HBFS_ECAPACITY, "single-GPU traversal supports n < 2^29");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g->mu);  // one traversal per graph workspace at a time
     if (g->wide)
         return run_bfs<uint64_t>(g, (uint32_t)root, p, parent, level, on_device, trace, trace_cap,
                                  n_layers, device_ms, st);
@@ -2017,6 +2018,7 @@ extern "C" int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows) {
     HB_ENTRY_BEGIN
     using namespace hbfs;
     if (!g || !out || rows < 0) return set_error(HBFS_EINVAL, "bad arguments");
+    std::lock_guard<std::mutex> lock(g->mu);
     if (!g->ws) return set_error(HBFS_EINVAL, "no traversal yet");
     if (rows > kRowsCap + 1) rows = kRowsCap + 1;
     HB_CUDA(cudaMemcpy(out, g->ws->phases.p, rows * kPhaseSlots * 8, cudaMemcpyDeviceToHost));

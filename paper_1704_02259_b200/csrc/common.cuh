@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include "../../include/hbfs.h"
@@ -136,6 +137,10 @@ struct hbfs_graph {
     hbfs::DevBuf adj;      // uint32[arcs + 8] (padded for aligned uint4 reads)
     hbfs::DevBuf posw;     // uint32[nw]: bit v = deg(v) > 0 (engine.py:29-57 `posw`)
     hbfs::Workspace *ws = nullptr;
+    // hbfs_bfs holds this for the whole call: the per-graph workspace (parent,
+    // level, bitmaps, queues, controller state, pinned trace mirror) serves one
+    // traversal at a time; concurrent callers on one graph serialise here.
+    std::mutex mu;
     ~hbfs_graph();
 };
 

@@ -6,6 +6,7 @@
 // reproduces numpy's stable argsort / key sort.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -190,6 +191,24 @@ __global__ void k_posw(int64_t n, int64_t nw, const OffT *rs, uint32_t *posw,
             if (mx) atomicMax(maxdeg, (unsigned long long)mx);
         }
     }
+}
+
+// Structural check of a caller-supplied CSR (hbfs_graph_from_csr, csr.load of a
+// cache blob): bit 0 row_starts[0] != 0, bit 1 row_starts decreases somewhere,
+// bit 2 an adjacency id >= n.  The traversal kernels index parent/level/bitmaps
+// by adjacency values, so a corrupt CSR must be refused, not traversed.
+__global__ void k_check_csr(int64_t n, int64_t arcs, const int64_t *rs, const uint32_t *adj,
+                            unsigned *bad) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned f = 0;
+    if (t0 == 0 && rs[0] != 0) f |= 1u;
+    for (int64_t i = t0; i < n; i += stride)
+        if (rs[i + 1] < rs[i]) f |= 2u;
+    for (int64_t i = t0; i < arcs; i += stride)
+        if ((int64_t)adj[i] >= n) f |= 4u;
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (f && (threadIdx.x & 31) == 0) atomicOr(bad, f);
 }
 
 __global__ void k_narrow(int64_t cnt, const int64_t *src, uint32_t *dst) {
@@ -547,6 +566,25 @@ extern "C" int hbfs_graph_from_csr(const int64_t *row_starts, const uint32_t *ad
         rc = set_error(HBFS_ECUDA, "row_starts copy failed");
     if (!rc && arcs > 0 && cudaMemcpyAsync(g->adj.p, adjacency, arcs * 4, kind, st) != cudaSuccess)
         rc = set_error(HBFS_ECUDA, "adjacency copy failed");
+    if (!rc) {
+        DevBuf bad;
+        unsigned hbad = 0;
+        rc = bad.alloc(4);
+        if (!rc && (cudaMemsetAsync(bad.p, 0, 4, st) != cudaSuccess))
+            rc = set_error(HBFS_ECUDA, "memset failed");
+        if (!rc) {
+            k_check_csr<<<grid_for(std::max<int64_t>(n, arcs)), 256, 0, st>>>(
+                n, arcs, rs64.as<int64_t>(), g->adj.as<uint32_t>(), bad.as<unsigned>());
+            if (cudaGetLastError() != cudaSuccess ||
+                cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                rc = set_error(HBFS_ECUDA, "CSR check failed");
+        }
+        if (!rc && hbad)
+            rc = set_error(HBFS_EINVAL, "invalid CSR:%s%s%s", (hbad & 1) ? " row_starts[0] != 0" : "",
+                           (hbad & 2) ? " row_starts not non-decreasing" : "",
+                           (hbad & 4) ? " adjacency id >= n" : "");
+    }
     if (!rc) {
         if (g->wide)
             cudaMemcpyAsync(g->rs.p, rs64.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, st);

@@ -78,3 +78,21 @@ extern "C" int hbfs_probe_random_sectors(int log_bytes, int log_region, double *
     return HBFS_OK;
     HB_ENTRY_END
 }
+
+// Tuning: the L2's DRAM fetch granularity for this context (cudaLimitMaxL2FetchGranularity,
+// 32..128 bytes).  previous (may be NULL) receives the value before the call; bytes < 0 only
+// queries.
+extern "C" int hbfs_l2_fetch_granularity(int bytes, int *previous) {
+    HB_ENTRY_BEGIN
+    using namespace hbfs;
+    clear_error();
+    size_t cur = 0;
+    HB_CUDA(cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity));
+    if (previous) *previous = (int)cur;
+    if (bytes >= 0) {
+        if (bytes > 128) return set_error(HBFS_EINVAL, "granularity must be <= 128 bytes");
+        HB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes));
+    }
+    return HBFS_OK;
+    HB_ENTRY_END
+}

@@ -192,6 +192,25 @@ def hybrid_bfs(g, source: int, p: HeuristicParams | None = None, cfg: VecConfig 
     return BfsTree(parent=parent, source=int(source)), trace
 
 
+def _check_device_out(t, name: str, n: int, dtypes) -> None:
+    """A device output buffer: CUDA tensor on the current device, shape (n,),
+    4-byte integer dtype, contiguous (the kernel writes n entries)."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"out {name}: expected a CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"out {name}: tensor is on {t.device}, not the current device")
+    if t.dtype not in dtypes or tuple(t.shape) != (n,) or not t.is_contiguous():
+        raise ValueError(f"out {name}: expected a contiguous {dtypes[0]} tensor of shape ({n},)")
+
+
+def _check_host_out(a, name: str, n: int, dtype) -> None:
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.shape != (n,) or \
+            not a.flags.c_contiguous or not a.flags.writeable:
+        raise ValueError(f"out {name}: expected a writable contiguous {np.dtype(dtype)} array of length {n}")
+
+
 def bfs(g, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = None,
         use_simd: bool = True, force_direction: str | None = None, parent_mode: str = "minid",
         device: bool = True, trace: bool = True, out=None) -> BfsResult:
@@ -212,6 +231,8 @@ def bfs(g, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = 
 
         if out is not None:
             parent, level = out
+            _check_device_out(parent, "parent", n, (torch.int32, getattr(torch, "uint32", torch.int32)))
+            _check_device_out(level, "level", n, (torch.int32,))
         else:
             parent = torch.empty(n, dtype=torch.int32, device="cuda")
             level = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -220,6 +241,8 @@ def bfs(g, root: int, p: HeuristicParams | None = None, cfg: VecConfig | None = 
     else:
         if out is not None:
             parent, level = out
+            _check_host_out(parent, "parent", n, np.uint32)
+            _check_host_out(level, "level", n, np.int32)
         else:
             parent = np.empty(n, dtype=np.uint32)
             level = np.empty(n, dtype=np.int32)

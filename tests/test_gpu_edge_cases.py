@@ -336,3 +336,96 @@ def test_byte_accounting_matches_model(cuda, small_golden, name):
                 dirs = [1 if x.direction == "bottom-up" else 0 for x in r.trace]
                 want = model(rs, adj, r.level.cpu().numpy(), dirs, rs_bytes=8 if g.wide_offsets else 4)
                 assert hb.traversal_bytes(g, s, r.level, r.trace) == want, (name, s, kw, p.heuristic)
+
+
+def test_bfs_out_buffers_checked(cuda):
+    """bfs(out=...) refuses buffers the kernel would overrun or misplace."""
+    import torch
+
+    hb = cuda
+    g, _, _ = graph(hb, [(0, 1), (1, 2), (2, 3)], 40)
+    n = g.num_vertices
+    good = (torch.empty(n, dtype=torch.int32, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda"))
+    hb.bfs(g, 0, out=good)
+    bad = [
+        (torch.empty(n - 1, dtype=torch.int32, device="cuda"), good[1]),   # too short
+        (good[0], torch.empty(n, dtype=torch.int64, device="cuda")),       # wrong dtype
+        (torch.empty(n, dtype=torch.int32), good[1]),                      # CPU tensor
+        (torch.empty(2 * n, dtype=torch.int32, device="cuda")[::2], good[1]),  # strided
+    ]
+    for b in bad:
+        with pytest.raises(ValueError):
+            hb.bfs(g, 0, out=b)
+    with pytest.raises(ValueError):
+        hb.bfs(g, 0, device=False, out=(np.empty(n - 1, np.uint32), np.empty(n, np.int32)))
+    with pytest.raises(ValueError):
+        hb.bfs(g, 0, device=False, out=(np.empty(n, np.int32), np.empty(n, np.int32)))
+
+
+def test_from_csr_rejects_corrupt(cuda):
+    """A foreign CSR (e.g. a damaged cache blob) is refused with ValueError
+    instead of being traversed out of bounds."""
+    hb = cuda
+    rs = np.array([0, 2, 3, 4], dtype=np.int64)
+    adj = np.array([1, 2, 0, 0], dtype=np.uint32)
+    hb.csr.from_csr(rs, adj).free()
+    for r, a in [(rs, np.array([1, 7, 0, 0], np.uint32)),         # id >= n
+                 (np.array([0, 3, 2, 4], np.int64), adj),         # decreasing
+                 (np.array([1, 2, 3, 4], np.int64), adj)]:        # rs[0] != 0
+        with pytest.raises(ValueError):
+            hb.csr.from_csr(r, a)
+
+
+def test_concurrent_calls_on_one_graph(cuda, oracle):
+    """hbfs_bfs serialises callers that share a graph workspace: traversals from
+    several threads at once all return their own root's exact result."""
+    import threading
+
+    hb = cuda
+    params = hb.GraphParams(scale=12, edgefactor=16, seed=3)
+    g = hb.generate_graph(params)
+    host = oracle.HostCsr(g.num_vertices, g.row_starts, g.adjacency, g.in_edges_total)
+    roots = [int(x) for x in hb.sample_sources(g, 16, 1)]
+    want = {s: oracle.bfs_reference(host, s)[1] for s in roots}
+    errors = []
+
+    def work(rs):
+        try:
+            for _ in range(3):
+                for s in rs:
+                    r = hb.bfs(g, s, device=False)
+                    if not np.array_equal(r.level, want[s]):
+                        errors.append(s)
+        except Exception as ex:  # pragma: no cover - reported below
+            errors.append(repr(ex))
+
+    ts = [threading.Thread(target=work, args=(roots[i::4],)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_imported_graph_released(cuda):
+    """as_device_graph frees a reference graph's device copy with the host graph."""
+    import gc
+
+    from paper_1704_02259_b200 import csr as C
+
+    hb = cuda
+
+    class RefLike:
+        def __init__(self):
+            self.row_starts = np.array([0, 1, 2], dtype=np.int64)
+            self.adjacency = np.array([1, 0], dtype=np.uint32)
+            self.in_edges_total = 1
+
+    h = RefLike()
+    tree, _ = hb.hybrid_bfs(h, 0)
+    assert list(tree.parent) == [0, 0]
+    dg = C.as_device_graph(h)
+    assert dg._h is not None and id(h) in C._IMPORTED
+    del h
+    gc.collect()
+    assert dg._h is None

@@ -60,6 +60,33 @@ def test_s24_kron_vs_reference_digests(cuda):
         assert sha(fl) == r["level_sha"] and sha(fp) == r["fifo_parent_sha"]
 
 
+def test_c4_kron_s26_graph_and_roots_vs_reference_digests(cuda):
+    """The headline graph: the device-built SCALE 26 CSR is byte-identical to
+    the graph the bench's reference arm traverses (the C oracle's generate +
+    csr_build, digests in hashes_s26.json from make_golden_s26.py), the 64
+    sampled roots equal the reference's sample_sources, and for 8 roots the
+    levels (reference bfs_reference), min-id parents and trace (reference
+    stock hybrid_bfs, alpha=14 beta=24, simd) match the reference's digests;
+    Beamer traversals (the bench's heuristic) give the same levels and parents."""
+    hb = cuda
+    with open(os.path.join(GOLDEN, "hashes_s26.json")) as fh:
+        rec = json.load(fh)["S26_kron"]
+    g = hb.generate_graph(hb.GraphParams(scale=26, edgefactor=16, seed=1))
+    assert (g.num_vertices, g.num_arcs, g.in_edges_total) == (rec["n"], rec["arcs"], rec["m"])
+    assert sha(g.row_starts) == rec["rs_sha"]
+    assert sha(g.adjacency) == rec["adj_sha"]
+    assert [int(x) for x in hb.sample_sources(g, 64, 1)] == rec["sources"]
+    assert len(rec["roots"]) >= 8
+    beamer = hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge")
+    for s, r in rec["roots"].items():
+        out = hb.bfs(g, int(s), hb.HeuristicParams(alpha=14, beta=24), use_simd=True, device=False)
+        assert sha(out.level) == r["level_sha"], s
+        assert sha(out.parent) == r["simd_a14b24"]["parent_sha"], s
+        assert trace_array(out.trace) == r["simd_a14b24"]["trace"], s
+        ob = hb.bfs(g, int(s), beamer, device=False)
+        assert sha(ob.level) == r["level_sha"] and sha(ob.parent) == r["simd_a14b24"]["parent_sha"], s
+
+
 def test_c4_kron_s26_vs_reference_kernels(cuda, oracle):
     hb = cuda
     from oracle import refnative
@@ -84,7 +111,7 @@ def test_c4_kron_s26_vs_reference_kernels(cuda, oracle):
 
 def test_s28_kron_one_gpu_vs_reference_kernel(cuda, oracle):
     """SCALE 28 (BASELINE config 5's graph, 2^33 arcs, 64-bit row offsets,
-    source-range CSR build) on one GPU: levels of one root against the
+    source-range CSR build) on one GPU: levels of two roots against the
     reference's compiled bfs_reference, parents against the min-id rule."""
     import torch
 
@@ -102,13 +129,14 @@ def test_s28_kron_one_gpu_vs_reference_kernel(cuda, oracle):
     assert nat is not None
     g = hb.generate_graph(hb.GraphParams(scale=28, edgefactor=16, seed=1))
     assert g.wide_offsets and g.num_arcs == 1 << 33
-    s = int(hb.sample_sources(g, 1, 1)[0])
-    out = hb.bfs(g, s, hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge"),
-                 device=False)
+    roots = [int(x) for x in hb.sample_sources(g, 2, 1)]
+    p = hb.HeuristicParams(alpha=14, beta=24, heuristic="beamer", counter_mode="edge")
+    outs = [hb.bfs(g, s, p, device=False) for s in roots]
     n = g.num_vertices
     rs, adj = g.row_starts, g.adjacency
     g.free()
-    _, ref_lev = nat.bfs_reference(rs, adj, n, s)
-    assert np.array_equal(out.level, ref_lev)
     host = oracle.HostCsr(n, rs, adj, 1 << 32)
-    assert np.array_equal(out.parent, oracle.minid_parents(host, ref_lev, s))
+    for s, out in zip(roots, outs):
+        _, ref_lev = nat.bfs_reference(rs, adj, n, s)
+        assert np.array_equal(out.level, ref_lev), s
+        assert np.array_equal(out.parent, oracle.minid_parents(host, ref_lev, s)), s

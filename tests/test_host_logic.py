@@ -138,3 +138,25 @@ def test_host_parent_result_arrays(monkeypatch):
     monkeypatch.setenv("HBFS_PINNED_RESULTS", "0")
     b = hybrid._host_parent(1 << 20)
     assert b.dtype == np.uint32 and b.shape == (1 << 20,) and b.base is None
+
+
+def test_reference_side_engine_registration():
+    """integration/hybfs_cuda.install adds "cuda" to the STOCK hybfs engine
+    table; on a host without a GPU, selecting it raises RuntimeError (no CPU
+    fallback), while the stock engines keep working."""
+    import torch
+
+    from oracle import refpkg
+
+    hybfs = refpkg.load()
+    if hybfs is None:
+        pytest.skip("oracle/_ref not built (needs /root/reference once)")
+    from integration import hybfs_cuda
+
+    hybfs_cuda.install(hybfs)
+    hybfs_cuda.install(hybfs)  # idempotent
+    assert hybfs.engine.ENGINES.count("cuda") == 1
+    assert hybfs.engine.resolve_engine("native") == "native"
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError):
+            hybfs.engine.resolve_engine("cuda")
