@@ -50,8 +50,8 @@ def _device_csr(g):
     hit = _graphs.get(id(g))
     if hit is not None and hit[0]() is g:
         return hit[1], hit[2]
-    rs = torch.from_numpy(np.ascontiguousarray(g.row_starts, dtype=np.int64)).cuda()
-    adj_np = np.ascontiguousarray(g.adjacency, dtype=np.uint32)
+    rs = torch.from_numpy(np.array(g.row_starts, dtype=np.int64)).cuda()  # writable copies
+    adj_np = np.array(g.adjacency, dtype=np.uint32)
     adj = torch.from_numpy(adj_np.view(np.int32)).cuda() if adj_np.size else \
         torch.zeros(1, dtype=torch.int32, device="cuda")
     key = id(g)

@@ -1686,7 +1686,7 @@ static int ws_alloc(hbfs_graph *g) {
         int vi = variant_index(n);
         if (vi < 0 || vi >= nv) vi = kDefaultVariant;
         w->fn = vt[vi].fn;
-        w->smem = dyn_smem_bytes<OffT>();
+        w->smem = dyn_smem_bytes<OffT>() + (size_t)env_i64("HBFS_SMEM_PAD", 0);  // experiment knob
         cudaError_t e = cudaFuncSetAttribute(w->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)w->smem);
         if (e == cudaSuccess)
