@@ -159,6 +159,15 @@ int hbfs_probe_random_sectors(int log_bytes, int log_region, double *gbs);
  * *previous (may be NULL) receives the old value. */
 int hbfs_l2_fetch_granularity(int bytes, int *previous);
 
+/* Debugging aids (compute-sanitizer substitutes, tools/sanitize.py):
+ * with HBFS_GUARD=1 in the environment every device buffer carries a guard
+ * band behind its end; hbfs_debug_guards checks all live bands (*clobbered =
+ * bands with a changed byte, *first_bytes = size of the first such buffer).
+ * hbfs_debug_checks reads the device index-check flags of a -DHBFS_CHECKED
+ * build (bit per check site; 0 = no violation) and optionally resets them. */
+int hbfs_debug_guards(int *enabled, int64_t *checked, int64_t *clobbered, int64_t *first_bytes);
+int hbfs_debug_checks(uint32_t *flags, int reset, int *is_checked_build);
+
 /* ---- per-layer steps on caller buffers: the hybfs._native surface ----
  * All pointers are DEVICE pointers in the reference's layout: rs int64[n+1],
  * adj uint32[arcs], LSB-first bitmaps uint32[ceil(n/32)] (frontier.py:3-6),

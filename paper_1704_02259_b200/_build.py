@@ -32,42 +32,58 @@ def _deps():
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    return _stale(LIB) or _stale(LIB_CHECKED)
+
+
+# The bounds-checked variant (device index checks, HB_DCHECK) that
+# tools/sanitize.py and tests/test_gpu_sanitize.py run in place of
+# compute-sanitizer, which the GPU pool does not allow.
+LIB_CHECKED = os.path.join(CSRC, "libhbfs_checked.so")
+VARIANTS = {LIB: ("build", []), LIB_CHECKED: ("build_checked", ["-DHBFS_CHECKED"])}
+
+
+def _stale(lib: str) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
-    objdir = os.path.join(CSRC, "build")
-    os.makedirs(objdir, exist_ok=True)
-    objs = []
-    procs = []
-    for src in sources():
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        objs.append(obj)
-        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
-            os.path.getmtime(p) for p in [src] + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(REPO, "include", "hbfs.h")]
-        ):
+    """Build libhbfs.so and libhbfs_checked.so (objects compiled in parallel)."""
+    jobs = []
+    for lib, (sub, extra) in VARIANTS.items():
+        if not force and not _stale(lib):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(REPO, "include"), "-c", src, "-o", obj]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
-    for src, p in procs:
-        out, _ = p.communicate()
-        if p.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{out[-6000:]}")
-        if verbose and out:
-            print(out)
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+        objdir = os.path.join(CSRC, sub)
+        os.makedirs(objdir, exist_ok=True)
+        objs = []
+        procs = []
+        for src in sources():
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            objs.append(obj)
+            if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
+                os.path.getmtime(p) for p in [src] + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(REPO, "include", "hbfs.h")]
+            ):
+                continue
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-c", src, "-o", obj]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+        jobs.append((lib, objs, procs))
+    for lib, objs, procs in jobs:
+        for src, p in procs:
+            out, _ = p.communicate()
+            if p.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {src}:\n{out[-6000:]}")
+            if verbose and out:
+                print(out)
+        tmp = lib + ".tmp"
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, lib)
     return LIB
 
 

@@ -72,6 +72,8 @@ SIGNATURES = {
     # multi-GPU partition (csrc/part.cu)
     "hbfs_probe_random_sectors": (C.c_int, [C.c_int, C.c_int, P]),
     "hbfs_l2_fetch_granularity": (C.c_int, [C.c_int, P]),
+    "hbfs_debug_guards": (C.c_int, [P, P, P, P]),
+    "hbfs_debug_checks": (C.c_int, [P, C.c_int, P]),
     "hbfs_layer_top_down": (C.c_int, [P, P, P, P, P, P, i64, P, P]),
     "hbfs_layer_bottom_up": (C.c_int, [P, P, P, P, P, P, i64, i32, P, P, P]),
     "hbfs_reference_bfs": (C.c_int, [P, P, i64, i64, P, P, P]),

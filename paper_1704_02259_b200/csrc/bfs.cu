@@ -75,6 +75,9 @@ constexpr int64_t kCbDefaultRanges = 16;
 // and harvest the next frontier from its bitmap (one extra barrier).
 constexpr int64_t kHarvestMinArcs = int64_t(1) << 22;
 
+// HB_DCHECK bits (checked builds): 0 parent/level index, 1 bitmap word,
+// 2 queue slot, 3 chunk-start slot, 4 adjacency index, 5 column-blocked
+// queue, 6 row-start index, 7 level-pass index
 struct Ctr {
     unsigned long long packed;  // discovered count << 35 | their degree sum
     unsigned long long gathers;
@@ -101,6 +104,7 @@ struct Queue {
     OffT *qo;      // exclusive degree prefix
     OffT *qr;      // row starts
     uint32_t *cs;  // chunk starts
+    int64_t cap, ncs;  // entries / chunk starts allocated (HB_DCHECK bounds)
 };
 
 template <typename OffT>
@@ -203,6 +207,7 @@ __device__ __forceinline__ void clear_spare_word(const A_t &A, int64_t L, int64_
     {
         const int32_t d = (int32_t)(L + 2 - kPlanes);
         while (x) {
+            HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
             A.level[w * 32 + __ffs(x) - 1] = d;
             x &= x - 1;
         }
@@ -314,13 +319,17 @@ __device__ __forceinline__ void block_enqueue(const bool (&claim)[I], const uint
         uint64_t c0 = 0, c1 = 0;
         const uint64_t mypos = pos;
         if (claim[k]) {
+            HB_DCHECK(pos < (uint64_t)Q.cap, 2);
             Q.q[pos] = v[k];
             Q.qo[pos] = (OffT)off;
             Q.qr[pos] = rsv[k];
             c0 = (off + kTdChunk - 1) / kTdChunk;
             c1 = (off + deg[k] + kTdChunk - 1) / kTdChunk;
             if (c1 - c0 <= 2)
-                for (uint64_t c = c0; c < c1; ++c) Q.cs[c] = (uint32_t)pos;
+                for (uint64_t c = c0; c < c1; ++c) {
+                    HB_DCHECK(c < (uint64_t)Q.ncs, 3);
+                    Q.cs[c] = (uint32_t)pos;
+                }
             ++pos;
             off += deg[k];
         }
@@ -331,7 +340,10 @@ __device__ __forceinline__ void block_enqueue(const bool (&claim)[I], const uint
             const uint64_t b0 = __shfl_sync(full, (unsigned long long)c0, src);
             const uint64_t b1 = __shfl_sync(full, (unsigned long long)c1, src);
             const uint32_t bp = (uint32_t)__shfl_sync(full, (unsigned long long)mypos, src);
-            for (uint64_t c = b0 + lane; c < b1; c += 32) Q.cs[c] = bp;
+            for (uint64_t c = b0 + lane; c < b1; c += 32) {
+                HB_DCHECK(c < (uint64_t)Q.ncs, 3);
+                Q.cs[c] = bp;
+            }
         }
     }
 }
@@ -692,7 +704,9 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
                     u[k] = Q.q[j];
                     rsu = Q.qr[j];
                 }
+                HB_DCHECK((uint64_t)rsu + (a - (uint64_t)off) < (uint64_t)A.arcs, 4);
                 v[k] = __ldg(A.adj + (uint64_t)rsu + (a - (uint64_t)off));
+                HB_DCHECK(v[k] < A.n && u[k] < A.n, 0);
             }
         }
         if (Harvest) {
@@ -799,6 +813,8 @@ __device__ __forceinline__ Queue<OffT> cb_queue(const Args<OffT> &A, int r, int6
     q.qo = A.cbq.qo + r * cb_max_f;
     q.qr = A.cbq.qr + r * cb_max_f;
     q.cs = A.cbq.cs + r * A.cb_cs_stride;
+    q.cap = cb_max_f;
+    q.ncs = A.cb_cs_stride;
     return q;
 }
 
@@ -839,11 +855,14 @@ __device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spa
                 atomicAdd(&A.ctl->cbctr[bank][lane], (1ull << kPackShift) + len);
             const uint64_t pos = old >> kPackShift, db = old & kPackMask;
             const Queue<OffT> R = cb_queue(A, lane, kCbMaxF);
+            HB_DCHECK(pos < (uint64_t)kCbMaxF, 5);
             R.q[pos] = u;
             R.qo[pos] = (OffT)db;
             R.qr[pos] = (OffT)((uint64_t)s + b);
-            for (uint64_t c = (db + kTdChunk - 1) / kTdChunk; c * kTdChunk < db + len; ++c)
+            for (uint64_t c = (db + kTdChunk - 1) / kTdChunk; c * kTdChunk < db + len; ++c) {
+                HB_DCHECK(c < (uint64_t)A.cb_cs_stride, 5);
                 R.cs[c] = (uint32_t)pos;
+            }
         }
     }
 }
@@ -971,8 +990,10 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 v[k] = (uint32_t)((tw + j) * 32 + bit);
                 s[k] = e[k] = 0;
                 if (act[k]) {
+                    HB_DCHECK(v[k] < A.n, 6);
                     s[k] = __ldg(A.rs + v[k]);
                     e[k] = __ldg(A.rs + v[k] + 1);
+                    HB_DCHECK(s[k] <= e[k] && (int64_t)e[k] <= A.arcs, 4);
                 }
             }
             int64_t hit[C];
@@ -986,6 +1007,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 const int64_t pos = found ? hit[k] - (int64_t)s[k] : -1;
                 const bool early = found && pos < max_pos;
                 if (found) {
+                    HB_DCHECK(v[k] < A.n && hu[k] < A.n && hit[k] < (int64_t)e[k] && hit[k] >= (int64_t)s[k], 0);
                     A.parent[v[k]] = hu[k];
                     if (A.direct_levels) A.level[v[k]] = (int32_t)S.layer + 1;
                     atomicOr(&s_found[(v[k] >> 5) - tw], 1u << (v[k] & 31));
@@ -1067,11 +1089,14 @@ __device__ __forceinline__ unsigned long long word_append(const Args<OffT> &A, c
         bits &= bits - 1;
         const OffT r0 = __ldg(A.rs + v);
         const uint64_t d = (uint64_t)(__ldg(A.rs + v + 1) - r0);
+        HB_DCHECK(pos < (uint64_t)Q.cap && v < A.n, 2);
         Q.q[pos] = v;
         Q.qo[pos] = (OffT)off;
         Q.qr[pos] = r0;
-        for (uint64_t c = (off + kTdChunk - 1) / kTdChunk; c * kTdChunk < off + d; ++c)
+        for (uint64_t c = (off + kTdChunk - 1) / kTdChunk; c * kTdChunk < off + d; ++c) {
+            HB_DCHECK(c < (uint64_t)Q.ncs, 3);
             Q.cs[c] = (uint32_t)pos;
+        }
         ++pos;
         off += d;
     }
@@ -1171,7 +1196,10 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
             vis[w] = vw[j] | bits[j];
             acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
             if (A.direct_levels)
-                for (uint32_t x = bits[j]; x; x &= x - 1) A.level[w * 32 + __ffs(x) - 1] = depth1;
+                for (uint32_t x = bits[j]; x; x &= x - 1) {
+                    HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
+                    A.level[w * 32 + __ffs(x) - 1] = depth1;
+                }
         }
     }
     acc = warp_sum(acc);
@@ -1302,11 +1330,13 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
                 }
                 const uint32_t hit = (((__shfl_sync(0xffffffffu, R, src) >> b0) & 0xFu) * 0x00204081u) & 0x01010101u;
                 v |= (hit ^ 0x01010101u) * 0xFFu;
+                HB_DCHECK((t * 32 + src) * 32 + 32 <= A.n, 7);
                 int4 *gdst = reinterpret_cast<int4 *>(A.level + (t * 32 + src) * 32);
                 __stcs(gdst + (lane & 7), make_int4(sext_byte<0>(v), sext_byte<1>(v), sext_byte<2>(v), sext_byte<3>(v)));
             }
         } else if (w < A.nw) {
             int32_t *dst = A.level + w * 32;
+            HB_DCHECK(w < A.nw, 7);
             for (int b = 0; b < 32; ++b) {
                 const int32_t lv = level_of(R, D, vw, d0, b);
                 if (w * 32 + b < A.n && lv != -2) dst[b] = lv;
@@ -1532,7 +1562,7 @@ __global__ void part_bu_counters(const Ctr *c, unsigned long long *out) {
 size_t part_bu_scratch_bytes() { return sizeof(Ctl) + 64; }
 
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local, int64_t n,
-                   int64_t lo, int64_t nloc, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
+                   int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st) {
     const int64_t wlo = lo >> 5, wown = (nloc + 31) / 32;
@@ -1544,6 +1574,7 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
     A.posw = posw_local - wlo;
     A.n = n;
     A.nw = (n + 31) / 32;
+    A.arcs = arcs_local;
     A.parent = parent_local - lo;
     A.level = level_local - lo;
     A.bits = V;
@@ -1746,6 +1777,8 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
         A.qb[b].qo = w->qo.as<OffT>() + b * (g->n + 1);
         A.qb[b].qr = w->qr.as<OffT>() + b * (g->n + 1);
         A.qb[b].cs = w->cs.as<uint32_t>() + b * w->ncs;
+        A.qb[b].cap = g->n + 1;
+        A.qb[b].ncs = w->ncs;
     }
     A.ctl = w->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(w->ctl.as<char>() + sizeof(Ctl));
@@ -1905,6 +1938,8 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
         A.qb[b].qo = T->qo.as<uint64_t>() + b * (nown + 1);
         A.qb[b].qr = T->qr.as<uint64_t>() + b * (nown + 1);
         A.qb[b].cs = T->cs.as<uint32_t>() + b * T->ncs;
+        A.qb[b].cap = nown + 1;
+        A.qb[b].ncs = T->ncs;
     }
     A.cbq.q = T->cbq.as<uint32_t>();
     A.cbq.qo = T->cbqo.as<uint64_t>();
@@ -2022,6 +2057,32 @@ extern "C" int hbfs_phase_times(hbfs_graph *g, uint64_t *out, int64_t rows) {
     if (!g->ws) return set_error(HBFS_EINVAL, "no traversal yet");
     if (rows > kRowsCap + 1) rows = kRowsCap + 1;
     HB_CUDA(cudaMemcpy(out, g->ws->phases.p, rows * kPhaseSlots * 8, cudaMemcpyDeviceToHost));
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// Device-side index-check flags of a -DHBFS_CHECKED build (bit per check
+// site of the traversal kernels, see HB_DCHECK and the bit legend at Ctr);
+// *is_checked_build = 0 and *flags = 0 otherwise.
+extern "C" int hbfs_debug_checks(uint32_t *flags, int reset, int *is_checked_build) {
+    HB_ENTRY_BEGIN
+    using namespace hbfs;
+    clear_error();
+#ifdef HBFS_CHECKED
+    if (is_checked_build) *is_checked_build = 1;
+    unsigned int f = 0;
+    HB_CUDA(cudaDeviceSynchronize());
+    HB_CUDA(cudaMemcpyFromSymbol(&f, g_check_fail, sizeof f));
+    if (flags) *flags = f;
+    if (reset) {
+        const unsigned int z = 0;
+        HB_CUDA(cudaMemcpyToSymbol(g_check_fail, &z, sizeof z));
+    }
+#else
+    (void)reset;
+    if (is_checked_build) *is_checked_build = 0;
+    if (flags) *flags = 0;
+#endif
     return HBFS_OK;
     HB_ENTRY_END
 }

@@ -25,6 +25,21 @@ void clear_error();
                                      cudaGetErrorString(e_));                           \
     } while (0)
 
+// Device-side index checks (builds with -DHBFS_CHECKED, the bounds-checked
+// variant tools/sanitize.py runs): a failed check sets bit `bit` of a device
+// flag word (read by hbfs_debug_checks) instead of trapping.
+#ifdef HBFS_CHECKED
+static __device__ unsigned int g_check_fail = 0;  // per translation unit (no rdc)
+#define HB_DCHECK(cond, bit)                                              \
+    do {                                                                  \
+        if (!(cond)) atomicOr(&::hbfs::g_check_fail, 1u << (bit));        \
+    } while (0)
+#else
+#define HB_DCHECK(cond, bit) \
+    do {                     \
+    } while (0)
+#endif
+
 #define HB_CHECK(expr)                    \
     do {                                  \
         int rc_ = (expr);                 \
@@ -49,6 +64,17 @@ constexpr int kBlock = HBFS_KBLOCK;  // threads per CTA for the traversal kernel
 
 struct Workspace;
 
+// Out-of-bounds write detection (compute-sanitizer is not available on the
+// GPU pool): with HBFS_GUARD=1 in the environment every DevBuf gets a guard
+// band of kGuardBytes filled with kGuardByte behind its end; hbfs_debug_guards
+// verifies every live band (a kernel that wrote past an array's end clobbers
+// it).  Off by default; no cost when off.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_enabled();
+void guard_register(void *p, size_t bytes);
+void guard_unregister(void *p);
+
 // Device block allocation helper (owned, freed in destructor).
 struct DevBuf {
     void *p = nullptr;
@@ -60,16 +86,24 @@ struct DevBuf {
     int alloc(size_t b) {
         release();
         if (b == 0) b = 16;
-        cudaError_t e = cudaMalloc(&p, b);
+        const bool guard = guard_enabled();
+        cudaError_t e = cudaMalloc(&p, b + (guard ? kGuardBytes : 0));
         if (e != cudaSuccess) {
             p = nullptr;
             return set_error(HBFS_ECAPACITY, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
         }
         bytes = b;
+        if (guard) {
+            cudaMemset(static_cast<char *>(p) + b, kGuardByte, kGuardBytes);
+            guard_register(p, b);
+        }
         return HBFS_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            guard_unregister(p);
+            cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -108,7 +142,7 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
 // (< 0: unknown).  scratch: part_bu_scratch_bytes() of device memory.
 size_t part_bu_scratch_bytes();
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local, int64_t n,
-                   int64_t lo, int64_t nloc, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
+                   int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st);
 

@@ -653,7 +653,7 @@ extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the persistent kernel's bottom-up tiles on the owned words (bfs.cu)
     HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->n, P->lo,
-                            P->nloc, P->F.as<uint32_t>(), P->V.as<uint32_t>(), P->parent.as<uint32_t>(),
+                            P->nloc, P->arcs, P->F.as<uint32_t>(), P->V.as<uint32_t>(), P->parent.as<uint32_t>(),
                             P->level.as<int32_t>(), next_slice, depth, max_pos, P->fhint, counters,
                             P->bu_scratch.p, st));
     return HBFS_OK;

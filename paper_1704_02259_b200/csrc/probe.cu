@@ -8,6 +8,12 @@
 // a large buffer and its 32 lanes each read one random 32-byte sector inside
 // it (two 16-byte loads, evict-first so L2 does not serve repeats).  bench.py
 // reports the result next to the copy-bandwidth roofline.
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
 #include "common.cuh"
 
 namespace hbfs {
@@ -96,3 +102,68 @@ extern "C" int hbfs_l2_fetch_granularity(int bytes, int *previous) {
     return HBFS_OK;
     HB_ENTRY_END
 }
+
+// ---- debugging aids (compute-sanitizer substitutes) ----
+
+namespace hbfs {
+
+namespace {
+std::mutex g_guard_mu;
+std::unordered_map<void *, size_t> &guards() {
+    static std::unordered_map<void *, size_t> m;
+    return m;
+}
+}  // namespace
+
+bool guard_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HBFS_GUARD");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
+void guard_register(void *p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    guards()[p] = bytes;
+}
+
+void guard_unregister(void *p) {
+    if (!guard_enabled()) return;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    guards().erase(p);
+}
+
+}  // namespace hbfs
+
+// Verify every live guard band: *clobbered = number of bands with a changed
+// byte; *first_bytes = the allocation size of the first clobbered buffer.
+extern "C" int hbfs_debug_guards(int *enabled, int64_t *checked, int64_t *clobbered, int64_t *first_bytes) {
+    HB_ENTRY_BEGIN
+    using namespace hbfs;
+    clear_error();
+    if (enabled) *enabled = guard_enabled() ? 1 : 0;
+    int64_t nchk = 0, nbad = 0, first = -1;
+    if (guard_enabled()) {
+        HB_CUDA(cudaDeviceSynchronize());
+        std::vector<unsigned char> h(kGuardBytes);
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        for (auto &kv : guards()) {
+            HB_CUDA(cudaMemcpy(h.data(), static_cast<char *>(kv.first) + kv.second, kGuardBytes,
+                               cudaMemcpyDeviceToHost));
+            ++nchk;
+            for (size_t i = 0; i < kGuardBytes; ++i)
+                if (h[i] != kGuardByte) {
+                    if (nbad == 0) first = (int64_t)kv.second;
+                    ++nbad;
+                    break;
+                }
+        }
+    }
+    if (checked) *checked = nchk;
+    if (clobbered) *clobbered = nbad;
+    if (first_bytes) *first_bytes = first;
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
