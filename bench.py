@@ -20,6 +20,9 @@ Extra keys:
                compiled engine, timed by hybfs.harness._run_one) on a bounded
                sample of distinct roots, concurrent worker processes
   clocks       nvidia-smi samples taken during the timed region
+  sub_configs  BASELINE configs[1] (Kronecker SCALE 20, the paper's size) and
+               configs[2] (uniform 2^22 / 2^26): value, roofline, e2e,
+               cpu_baseline measured the same way in the same run
 
 --impl reference runs the reference's CPU path instead (rank 0 only).
 """
@@ -72,6 +75,8 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parent-mode", choices=("minid", "any"), default="minid")
+    ap.add_argument("--no-sub-configs", action="store_true",
+                    help="skip the configs[1]/[2] (SCALE 20, uniform 2^22) sub-results of the default line")
     return ap.parse_args()
 
 
@@ -293,20 +298,29 @@ def cpu_baseline_for(cfg, g):
 
 # -------------------------------------------------------------------- ours
 
-def run_ours(args, cfg):
-    import numpy as np
+def pcie_d2h_gbs(nbytes: int) -> float:
+    """Live pinned device->host copy rate (GB/s) for an nbytes result array."""
+    import torch
+
+    src = torch.empty(nbytes // 4, dtype=torch.int32, device="cuda")
+    dst = torch.empty(nbytes // 4, dtype=torch.int32, pin_memory=True)
+    best = float("inf")
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return nbytes / best / 1e9
+
+
+def measure_config(args, cfg, steps, warmup, with_cpu_baseline, dist_world=1):
+    """The bench line's measurements for one BASELINE config on this GPU."""
     import torch
 
     import paper_1704_02259_b200 as hb
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        torch.cuda.set_device(local)
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", torch.cuda.current_device())
-
     params = hb.GraphParams(scale=cfg["scale"], edgefactor=16, seed=1, probs=cfg["probs"])
     g = hb.generate_graph(params)
     roots = hb.sample_sources(g, ROOTS, 1)
@@ -316,44 +330,39 @@ def run_ours(args, cfg):
     level = torch.empty(n, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def sweep(record):
+    def sweep():
         times = []
         for s in roots:
             flush.fill_(1)
             r = hb.bfs(g, int(s), p, use_simd=True, parent_mode=args.parent_mode, device=True,
-                       trace=record, out=(parent, level))
+                       trace=False, out=(parent, level))
             times.append(r.device_seconds)
-            if record:
-                record.append(r.trace)
         return times
 
-    for _ in range(args.warmup):
-        sweep(None)
-    if ws > 1:
+    for _ in range(warmup):
+        sweep()
+    if dist_world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     per_root = [[] for _ in roots]
     launches = 0
     with ClockSampler(dev.index) as clk:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            tr = []
-            ts = sweep(tr)
-            for i, t in enumerate(ts):
+        for _ in range(steps):
+            for i, t in enumerate(sweep()):
                 per_root[i].append(t)
             # per traversal: the persistent bfs_kernel, plus levels_kernel when
             # levels are stamped from the depth planes (n >= 2^22, csrc/bfs.cu)
-            launches += len(ts) * (2 if n >= (1 << 22) else 1)
+            launches += len(roots) * (2 if n >= (1 << 22) else 1)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     total_dev = sum(sum(x) for x in per_root)
-    if ws > 1:
+    if dist_world > 1:
         t = torch.tensor([total_dev], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_dev = float(t.item())
-    traversals = len(roots) * args.steps
-    value = ws * traversals * m / total_dev / 1e9
-    ms_per_step = total_dev / args.steps * 1e3
+    traversals = len(roots) * steps
+    value = dist_world * traversals * m / total_dev / 1e9
 
     # --- validation + byte accounting (untimed), one pass over the roots
     invalid = 0
@@ -371,61 +380,120 @@ def run_ours(args, cfg):
     peak, peak_src = measured_peak()
     achieved = b_sector / t_roots / 1e9
     traffic = profiled_traffic(cfg["label"])
-    rnd = random_sector_ceiling()
 
-    # --- e2e: the reference-facing call, hybrid_bfs(g, s) -> (BfsTree, trace), exactly as
-    # a user makes it (kernel + trace + D2H of the parent array into the host result,
-    # which hybrid_bfs takes from the pinned caching allocator)
-    e2e_secs = []
-    hb.hybrid_bfs(g, int(roots[0]), p, use_simd=True, engine_name="cuda",
-                  parent_mode=args.parent_mode)  # warm-up: fills the pinned-block cache
-    for s in roots:
-        flush.fill_(1)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        tree, _ = hb.hybrid_bfs(g, int(s), p, use_simd=True, engine_name="cuda",
-                                parent_mode=args.parent_mode)
-        assert tree.parent[int(s)] == int(s)
-        del tree
-        e2e_secs.append(time.perf_counter() - t1)
-    e2e_value = len(e2e_secs) * m / sum(e2e_secs) / 1e9
+    # --- e2e through the reference-facing calls, host wall clock per root:
+    # (1) hybrid_bfs(g, s) -> (BfsTree parents on the host, trace): the
+    #     reference's own return value (its BfsTree carries no levels);
+    # (2) bfs(g, s, device=False) -> parents AND levels on the host.
+    # L2 flushed before each call (outside the clock).
+    def e2e(call):
+        call(int(roots[0]))  # warm-up: pinned-block cache
+        secs = []
+        for s in roots:
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            call(int(s))
+            secs.append(time.perf_counter() - t1)
+        return len(secs) * m / sum(secs) / 1e9, sum(secs) / len(secs)
 
-    if rank != 0:
-        return 0
-    line = {
-        "metric": "harmonic-mean GTEPS over 64 roots",
-        "value": value, "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (bit-exact reference R-MAT generator on device, seed 1)",
+    def call_tree(s):
+        tree, _ = hb.hybrid_bfs(g, s, p, use_simd=True, engine_name="cuda", parent_mode=args.parent_mode)
+        assert tree.parent[s] == s
+
+    host_par = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    host_lev = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+
+    def call_both(s):
+        r = hb.bfs(g, s, p, use_simd=True, parent_mode=args.parent_mode, device=False, out=(host_par, host_lev))
+        assert r.level[s] == 0
+
+    e_tree, t_tree = e2e(call_tree)
+    e_both, t_both = e2e(call_both)
+    d2h = pcie_d2h_gbs(4 * n)
+    t_dev = t_roots / len(roots)
+    out = {
+        "value": value, "ms_per_step": total_dev / steps * 1e3, "wall_s_timed_region": wall,
+        "gpu_launches": launches, "clocks": clk.summary(),
         "config": {"workload": cfg["label"], "scale": cfg["scale"], "edgefactor": 16,
                    "roots": ROOTS, "heuristic": cfg["heur"], "parent_mode": args.parent_mode,
-                   "parallelism": "replicas" if ws > 1 else "single-gpu",
                    "l2": "flushed (256 MB write) before every traversal", "m_edges": m,
                    "arcs": g.num_arcs, "invalid_trees": invalid},
-        "gpu_launches": launches,
-        "wall_s_timed_region": wall,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "bfs_kernel (persistent, one launch per traversal; + levels_kernel)",
                      "bytes_per_launch": b_sector / len(roots),
                      "useful_bytes_per_launch": b_useful / len(roots),
-                     "launch_ms": t_roots / len(roots) * 1e3, "peak_source": peak_src,
-                     "random_sector_gbs": rnd,
+                     "launch_ms": t_dev * 1e3, "peak_source": peak_src},
+        "e2e": {"value": e_tree, "unit": "GTEPS", "h2d_bytes_per_step": 8 * len(roots),
+                "d2h_bytes_per_step": len(roots) * (4 * n + 256),
+                "call": "hybrid_bfs(g, root) per root: BfsTree parents (host) + trace",
+                "parents_and_levels": {
+                    "value": e_both, "unit": "GTEPS", "d2h_bytes_per_step": len(roots) * (8 * n + 256),
+                    "call": "bfs(g, root, device=False): parent and level arrays (host) + trace"},
+                "pcie_d2h_gbs": d2h,
+                "ceiling_note": "per root = traversal + D2H of the result at the measured pinned copy rate",
+                "ceiling_gteps": {"parents": m / (t_dev + 4 * n / (d2h * 1e9)) / 1e9,
+                                  "parents_and_levels": m / (t_dev + 8 * n / (d2h * 1e9)) / 1e9},
+                "ms_per_root": {"device": t_dev * 1e3, "parents": t_tree * 1e3, "parents_and_levels": t_both * 1e3}},
+    }
+    if with_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline_for(cfg, g)
+        except Exception as ex:  # the product line must still print
+            out["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
+    g.free()
+    del parent, level, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+SUB_CONFIGS = ("c2", "c3")  # BASELINE configs[1] (the paper's SCALE 20) and [2] (uniform)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    main = measure_config(args, cfg, args.steps, args.warmup, ws == 1 and not args.no_cpu_baseline, ws)
+    subs = {}
+    if args.config == DEFAULT_CONFIG and not args.no_sub_configs:
+        for name in SUB_CONFIGS:
+            sc = CONFIGS[name]
+            r = measure_config(args, sc, max(args.steps, 3), max(args.warmup, 3),
+                               ws == 1 and not args.no_cpu_baseline, ws)
+            subs[name] = {k: r[k] for k in ("value", "ms_per_step", "config", "roofline", "e2e", "cpu_baseline",
+                                            "clocks") if k in r}
+            subs[name]["unit"] = "GTEPS"
+    if rank != 0:
+        return 0
+    rnd = random_sector_ceiling()
+    line = {
+        "metric": "harmonic-mean GTEPS over 64 roots",
+        "value": main["value"], "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (bit-exact reference R-MAT generator on device, seed 1)",
+        "config": {**main["config"], "parallelism": "replicas" if ws > 1 else "single-gpu"},
+        "gpu_launches": main["gpu_launches"],
+        "wall_s_timed_region": main["wall_s_timed_region"],
+        "roofline": {**main["roofline"], "random_sector_gbs": rnd,
                      "random_sector_note": "measured live: random 32-byte sector reads of an 8 GiB buffer, "
                                            "each warp inside one random 256 KiB region (the gathers' pattern) "
                                            "and uniformly random; the attainable ceiling for data-dependent "
                                            "sector traffic, next to the copy-bandwidth peak"},
-        "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 4 * len(roots),
-                "d2h_bytes_per_step": len(roots) * (4 * n + 256),
-                "call": "hybrid_bfs(g, root) per root: BfsTree parents (host) + trace"},
-        "clocks": clk.summary(),
+        "e2e": main["e2e"],
+        "clocks": main["clocks"],
     }
-    if ws == 1 and not args.no_cpu_baseline:
-        try:
-            line["cpu_baseline"] = cpu_baseline_for(cfg, g)
-        except Exception as ex:  # the product line must still print
-            line["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
+    if "cpu_baseline" in main:
+        line["cpu_baseline"] = main["cpu_baseline"]
+    if subs:
+        line["sub_configs"] = subs
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
