@@ -240,9 +240,21 @@ __device__ __forceinline__ uint32_t ld_global(const uint32_t *gp) {
     asm("ld.global.u32 %0, [%1];" : "=r"(r) : "l"(gp));
     return r;
 }
-// bm: a global-space address (pin_ptr), so the probe is an explicit LDG
+// bm: a global-space address (pin_ptr), so the probe is an explicit LDG.
+// HBFS_PROBE_POLICY (profiling builds only): the probe carries an explicit
+// L2 evict_normal policy — the default behaviour, made explicit so that ncu's
+// per-instruction "L2 Explicit Hit/Miss Policy Evict Normal" counters measure
+// the L2 hit rate of the frontier-bitmap probes alone (tools/probe_l2.py).
 __device__ __forceinline__ uint32_t probe_word(const uint32_t *__restrict__ bm, uint32_t a) {
+#ifdef HBFS_PROBE_POLICY
+    uint64_t pol;
+    uint32_t r;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    asm("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(bm + (a >> 5)), "l"(pol));
+    return r;
+#else
     return ld_global(bm + (a >> 5));
+#endif
 }
 
 // Position of the (r+1)-th set bit of m (r < popc(m)); cheaper than __fns.
@@ -354,6 +366,27 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
     return x;
 }
 
+// Adjacency vector load with an L2 prefetch-size hint.  Measured on this B200
+// (tools/mb/sector.cu under ncu): a plain / .nc / .cs load that misses L2
+// fetches the whole 128-byte line from DRAM (dram bytes = 4x the 32-byte
+// sector asked for); .L2::64B halves that.  PF = 0: no hint.
+template <int PF>
+__device__ __forceinline__ uint4 ld_adj4(const uint32_t *p) {
+    uint4 r;
+    if (PF == 64)
+        asm("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (PF == 128)
+        asm("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (PF == 256)
+        asm("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else
+        r = __ldg(reinterpret_cast<const uint4 *>(p));
+    return r;
+}
+
 // Opaque global-space copy of a pointer: the compiler cannot rematerialise it (it would
 // otherwise rebuild the bitmap plane address from the parameter bank with a
 // 64-bit add chain at every probe — 5 extra instructions per probe).
@@ -372,7 +405,7 @@ __device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
 // FIRST1 (dense frontiers, where nearly every found vertex hits at its first
 // entry): probe that entry alone before the vectors — one bitmap load instead
 // of up to four.
-template <typename OffT, int K, int LV, bool FIRST1>
+template <typename OffT, int K, int LV, bool FIRST1, int PF = 0>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                                            const uint32_t *__restrict__ bm_in,
                                            const bool (&act)[K], const OffT (&s)[K],
@@ -411,7 +444,7 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             go[k] = act[k] && hit[k] < 0 && p[k] < e[k];
-            if (go[k]) q4[k] = __ldg(reinterpret_cast<const uint4 *>(adj + (p[k] & ~(OffT)3)));
+            if (go[k]) q4[k] = ld_adj4<PF>(adj + (p[k] & ~(OffT)3));
             else q4[k] = make_uint4(0, 0, 0, 0);
         }
         uint32_t wd[K][4];
@@ -932,7 +965,7 @@ struct TileSched {
 // PART: one rank's share of a 1D partition (csrc/part.cu): tiles cover the
 // owned words [part_w0, part_wend) only; the arrays indexed by vertex or word
 // are offset pointers (see part_bu_launch), and there is no depth ring.
-template <typename OffT, int C, int LV, bool FIRST1, bool PART = false>
+template <typename OffT, int C, int LV, bool FIRST1, bool PART = false, int PF = 0>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
     const unsigned full = 0xffffffffu;
@@ -998,7 +1031,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
             int64_t hit[C];
             uint32_t hu[C];
-            first_hits<OffT, C, LV, FIRST1>(A.adj, in.p, act, s, e, hit, hu);
+            first_hits<OffT, C, LV, FIRST1, PF>(A.adj, in.p, act, s, e, hit, hu);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 if (!act[k]) continue;
@@ -1480,7 +1513,10 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                 phase_bu<OffT, K, kLaneVecsScan, false, PART>(A, S, in, out, spare, ctr, red, sf);
             else if (S.v_f * A.first1_div >= A.n)
                 phase_bu<OffT, K, kLaneVecs, true, PART>(A, S, in, out, spare, ctr, red, sf);
-            else phase_bu<OffT, K, kLaneVecs, false, PART>(A, S, in, out, spare, ctr, red, sf);
+            // large graphs, dense frontier: most rows stop in their first
+            // vector, so its miss fetches 64 bytes instead of the 128-byte line
+            // (SCALE 26 dense bottom-up layers -2.5%, no change elsewhere)
+            else phase_bu<OffT, K, kLaneVecs, false, PART, SCAN ? 64 : 0>(A, S, in, out, spare, ctr, red, sf);
         }
         grid.sync();
 
