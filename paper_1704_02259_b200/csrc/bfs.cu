@@ -48,11 +48,6 @@ constexpr int kLaneVecs = 2;
 constexpr int kLaneVecsScan = 4;
 constexpr int kTdMaxSub = 8;  // top-down chunk split on small layers (2048 / 8 = 256 arcs per CTA)
 constexpr uint64_t kTailLong = 256;  // open rows longer than this use the whole-warp scan
-// Single first probe when the frontier holds >= n/16 vertices — on graphs
-// without hubs (max degree < 64x the mean, e.g. uniform): there it saves
-// probe traffic (uniform 2^22: +7%); on Kronecker graphs the extra dependent
-// step costs more than the saved probes (SCALE 20: -6%).
-constexpr int64_t kFirst1Div = 16;
 constexpr int kPackShift = 35;               // packed counter: count<<35 | degree sum
 constexpr unsigned long long kPackMask = (1ull << kPackShift) - 1;
 constexpr int64_t kRowsCap = 1024;           // trace rows per launch
@@ -112,6 +107,7 @@ struct Args {
     const OffT *rs;
     const uint32_t *adj;
     const uint32_t *posw;
+    const uint4 *hd;  // head records (common.cuh), indexed like rs
     int64_t n, nw, arcs, ncs;
     uint32_t *parent;
     int32_t *level;
@@ -127,7 +123,6 @@ struct Args {
     Heur H;
     int max_pos, use_simd, parent_mode, do_init;
     int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
-    int64_t first1_div;  // bottom-up probes a row's first entry alone when v_f >= n / first1_div
     int64_t part_w0, part_wend;  // partition (PART): owned word range
     int64_t part_lo, part_nown;  // partition (PART): owned vertex range
     uint32_t *cand, *touch;      // partition top-down: remote targets' min parent / touched bits
@@ -938,13 +933,20 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
 // Bottom-up layer.  A warp takes a tile of 32 bitmap words (one per lane), so
 // finished words are skipped 32 at a time.  The tile's candidates (unvisited,
 // degree > 0) are compacted across the lanes — every lane works regardless of
-// how candidates are spread over words — and each lane runs C independent
-// first-hit searches at once (first_hits: uint4 row probes against the
-// frontier bitmap, warp-cooperative scan for long rows).  Found bits gather in
-// the warp's shared-memory copy of the tile, then one plain store per word
-// updates out/vis (the warp owns its words).  Counters gathers/fallbacks are
-// those of the reference's 16-lane kernel.  Replaces
-// bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
+// how candidates are spread over words — and each lane resolves C candidates
+// at once from their 16-byte head records (common.cuh: degree + the first
+// kHeadLen row entries): one record load and up to kHeadLen probes of the
+// frontier bitmap decide "first hit at position j < kHeadLen" or "row ends
+// inside the head, no parent in this layer" without touching the row starts
+// or the adjacency array (SCALE 26: 80-99% of the candidates of every
+// bottom-up layer, tools/headstats.py).  Candidates still open are pushed on
+// a per-warp shared-memory list and drained 32 at a time (one row per lane,
+// all lanes busy) by first_hits from row position kHeadLen: uint4 row probes,
+// warp-cooperative scan for long rows — the reference's first-hit rule.
+// Found bits gather in the warp's shared-memory copy of the tile, then one
+// plain store per word updates out/vis (the warp owns its words).  Counters
+// gathers/fallbacks are those of the reference's 16-lane kernel.
+// Replaces bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
 // bu_probe.h:22-106).
 // Warp tile scheduler: the first tile is the warp's own index (no atomic, so
 // short layers spread over all warps), then one tile per atomic grab from a
@@ -962,20 +964,71 @@ struct TileSched {
     }
 };
 
+constexpr int kOpenCap = 64;  // open-list entries per warp: < 32 pending + one push of <= 32
+
+// Per-thread packed counters of a bottom-up layer:
+// fd = found << 35 | their degree sum; fg = fallbacks << 35 | gathers.
+struct BuCount {
+    unsigned long long fd = 0, fg = 0;
+    __device__ __forceinline__ void add(bool found, int64_t pos, int64_t deg, int64_t max_pos) {
+        const bool early = found && pos < max_pos;
+        if (found) fd += (1ull << kPackShift) + (unsigned long long)deg;
+        fg += (unsigned long long)(early ? pos + 1 : (deg < max_pos ? deg : max_pos));
+        if (deg > max_pos && !early) fg += 1ull << kPackShift;
+    }
+};
+
+// Drain up to 32 open candidates (v, degree) from the top of the warp's list:
+// lane i continues row i at position kHeadLen.
+template <typename OffT, int LV, int PF>
+__device__ __forceinline__ void bu_drain(const Args<OffT> &A, const uint32_t *bm_in, uint2 *ol,
+                                         uint32_t &nopen, int64_t tw, uint32_t *s_found,
+                                         int64_t max_pos, int32_t depth1, BuCount &cnt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t take = nopen < 32u ? nopen : 32u;
+    nopen -= take;
+    const bool act[1] = {(uint32_t)lane < take};
+    const uint2 ent = act[0] ? ol[nopen + lane] : make_uint2(0u, 0u);
+    OffT r0 = 0;
+    if (act[0]) {
+        HB_DCHECK(ent.x < A.n, 6);
+        r0 = __ldg(A.rs + ent.x);
+        HB_DCHECK((int64_t)r0 + ent.y <= A.arcs, 4);
+    }
+    const OffT s[1] = {(OffT)(r0 + kHeadLen)}, e[1] = {(OffT)(r0 + ent.y)};
+    int64_t hit[1];
+    uint32_t hu[1];
+    first_hits<OffT, 1, LV, false, PF>(A.adj, bm_in, act, s, e, hit, hu);
+    if (act[0]) {
+        const bool found = hit[0] >= 0;
+        if (found) {
+            HB_DCHECK(hu[0] < A.n && hit[0] < (int64_t)e[0] && hit[0] >= (int64_t)s[0], 0);
+            A.parent[ent.x] = hu[0];
+            if (A.direct_levels) A.level[ent.x] = depth1;
+            atomicOr(&s_found[(ent.x >> 5) - tw], 1u << (ent.x & 31));
+        }
+        cnt.add(found, found ? hit[0] - (int64_t)r0 : -1, (int64_t)ent.y, max_pos);
+    }
+    __syncwarp();  // the list slots just read may be pushed over
+}
+
 // PART: one rank's share of a 1D partition (csrc/part.cu): tiles cover the
 // owned words [part_w0, part_wend) only; the arrays indexed by vertex or word
 // are offset pointers (see part_bu_launch), and there is no depth ring.
-template <typename OffT, int C, int LV, bool FIRST1, bool PART = false, int PF = 0>
+template <typename OffT, int C, int LV, bool PART = false, int PF = 0>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
-                         const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found) {
+                         const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found,
+                         uint2 *ol) {
     const unsigned full = 0xffffffffu;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const Plane vis{A.bits};
     const int64_t max_pos = A.max_pos;
-    // packed per-thread counters: found<<35 | their degree sum ; fallbacks<<35 | gathers
-    unsigned long long c_fd = 0, c_fg = 0;
+    const int32_t depth1 = (int32_t)S.layer + 1;
+    const uint32_t *__restrict__ bm = pin_ptr(in.p);
+    BuCount cnt;
     const int64_t w0 = PART ? A.part_w0 : 0, wend = PART ? A.part_wend : A.nw;
     const int64_t ntiles = (wend - w0 + 31) >> 5;
 
@@ -1002,10 +1055,11 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         if (T == 0) continue;
         s_found[lane] = 0;
         __syncwarp();
+        uint32_t nopen = 0;  // warp-uniform
         for (uint32_t b = 0; b < T; b += 32 * C) {
             bool act[C];
-            OffT s[C], e[C];
             uint32_t v[C];
+            uint4 h[C];
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const uint32_t c = b + k * 32 + lane;
@@ -1021,35 +1075,55 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                 const uint32_t ex = __shfl_sync(full, incl, j) - __shfl_sync(full, cntl, j);
                 const uint32_t bit = act[k] ? nth_bit(cm, c - ex) : 0u;
                 v[k] = (uint32_t)((tw + j) * 32 + bit);
-                s[k] = e[k] = 0;
+                h[k] = make_uint4(0u, 0u, 0u, 0u);
                 if (act[k]) {
                     HB_DCHECK(v[k] < A.n, 6);
-                    s[k] = __ldg(A.rs + v[k]);
-                    e[k] = __ldg(A.rs + v[k] + 1);
-                    HB_DCHECK(s[k] <= e[k] && (int64_t)e[k] <= A.arcs, 4);
+                    h[k] = __ldg(A.hd + v[k]);
                 }
             }
-            int64_t hit[C];
-            uint32_t hu[C];
-            first_hits<OffT, C, LV, FIRST1, PF>(A.adj, in.p, act, s, e, hit, hu);
+            // Probes in two steps: the first head entry alone (it decides most
+            // candidates), the other two only where it missed — a probe is a
+            // random L2 sector request, and the SM's request rate (about one
+            // sector per clock) is what bounds a dense bottom-up layer.
+            uint32_t pw[C][kHeadLen];
+#pragma unroll
+            for (int k = 0; k < C; ++k)  // degree 0 when inactive: no probe
+                pw[k][0] = h[k].x > 0 ? probe_word(bm, h[k].y) : 0u;
 #pragma unroll
             for (int k = 0; k < C; ++k) {
-                if (!act[k]) continue;
-                const bool found = hit[k] >= 0;
-                const int64_t deg = (int64_t)(e[k] - s[k]);
-                const int64_t pos = found ? hit[k] - (int64_t)s[k] : -1;
-                const bool early = found && pos < max_pos;
-                if (found) {
-                    HB_DCHECK(v[k] < A.n && hu[k] < A.n && hit[k] < (int64_t)e[k] && hit[k] >= (int64_t)s[k], 0);
-                    A.parent[v[k]] = hu[k];
-                    if (A.direct_levels) A.level[v[k]] = (int32_t)S.layer + 1;
-                    atomicOr(&s_found[(v[k] >> 5) - tw], 1u << (v[k] & 31));
-                    c_fd += (1ull << kPackShift) + (unsigned long long)deg;
+                const bool more = !((pw[k][0] >> (h[k].y & 31)) & 1u);
+                pw[k][1] = more && h[k].x > 1 ? probe_word(bm, h[k].z) : 0u;
+                pw[k][2] = more && h[k].x > 2 ? probe_word(bm, h[k].w) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const uint32_t hm = ((pw[k][0] >> (h[k].y & 31)) & 1u) |
+                                    (((pw[k][1] >> (h[k].z & 31)) & 1u) << 1) |
+                                    (((pw[k][2] >> (h[k].w & 31)) & 1u) << 2);
+                const bool found = hm != 0;
+                const bool open = act[k] && !found && h[k].x > (uint32_t)kHeadLen;
+                if (act[k] && !open) {
+                    const int j = __ffs(hm) - 1;  // -1: not found
+                    if (found) {
+                        const uint32_t hu = j == 0 ? h[k].y : j == 1 ? h[k].z : h[k].w;
+                        HB_DCHECK(hu < A.n, 0);
+                        A.parent[v[k]] = hu;
+                        if (A.direct_levels) A.level[v[k]] = depth1;
+                        atomicOr(&s_found[(v[k] >> 5) - tw], 1u << (v[k] & 31));
+                    }
+                    cnt.add(found, (int64_t)j, (int64_t)h[k].x, max_pos);
                 }
-                c_fg += (unsigned long long)(early ? pos + 1 : (deg < max_pos ? deg : max_pos));
-                if (deg > max_pos && !early) c_fg += 1ull << kPackShift;
+                const unsigned m = __ballot_sync(full, open);
+                if (m) {
+                    if (open) ol[nopen + __popc(m & lt)] = make_uint2(v[k], h[k].x);
+                    nopen += __popc(m);
+                    __syncwarp();
+                    if (nopen >= 32u)
+                        bu_drain<OffT, LV, PF>(A, in.p, ol, nopen, tw, s_found, max_pos, depth1, cnt);
+                }
             }
         }
+        while (nopen) bu_drain<OffT, LV, PF>(A, in.p, ol, nopen, tw, s_found, max_pos, depth1, cnt);
         __syncwarp();
         const uint32_t f = s_found[lane];
         if (valid && f) {
@@ -1059,8 +1133,8 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         __syncwarp();
     }
     // CTA reduction of the counters, one atomic per CTA per counter.
-    c_fd = warp_sum(c_fd);
-    c_fg = warp_sum(c_fg);
+    unsigned long long c_fd = warp_sum(cnt.fd);
+    unsigned long long c_fg = warp_sum(cnt.fg);
     const int wid = threadIdx.x >> 5;
     if (lane == 0) {
         red[wid * 2 + 0] = c_fd;
@@ -1509,14 +1583,11 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                     if (x && (vis_all[w] & x) != x) vis_all[w] |= x;
                 }
             }
-            if (SCAN && S.v_f * 64 < A.n)
-                phase_bu<OffT, K, kLaneVecsScan, false, PART>(A, S, in, out, spare, ctr, red, sf);
-            else if (S.v_f * A.first1_div >= A.n)
-                phase_bu<OffT, K, kLaneVecs, true, PART>(A, S, in, out, spare, ctr, red, sf);
-            // large graphs, dense frontier: most rows stop in their first
-            // vector, so its miss fetches 64 bytes instead of the 128-byte line
-            // (SCALE 26 dense bottom-up layers -2.5%, no change elsewhere)
-            else phase_bu<OffT, K, kLaneVecs, false, PART, SCAN ? 64 : 0>(A, S, in, out, spare, ctr, red, sf);
+            uint2 *ol = reinterpret_cast<uint2 *>(dsm) + (threadIdx.x >> 5) * kOpenCap;  // TdSmem is idle
+            if (SCAN && S.v_f * 64 < A.n)  // tiny frontier: open rows are mostly scanned to their end
+                phase_bu<OffT, K, kLaneVecsScan, PART>(A, S, in, out, spare, ctr, red, sf, ol);
+            else
+                phase_bu<OffT, K, kLaneVecs, PART>(A, S, in, out, spare, ctr, red, sf, ol);
         }
         grid.sync();
 
@@ -1583,8 +1654,9 @@ __global__ void __launch_bounds__(kBlock, 2) part_bu_kernel(Args<OffT> A, St S, 
                                                           uint32_t *outp) {
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];
-    phase_bu<OffT, K, LV, false, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
-                                       ctr, red, s_found + (threadIdx.x & ~31));
+    __shared__ uint2 s_open[(kBlock / 32) * kOpenCap];
+    phase_bu<OffT, K, LV, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
+                                ctr, red, s_found + (threadIdx.x & ~31), s_open + (threadIdx.x >> 5) * kOpenCap);
 }
 
 // Ctr (found << 35 | degree sum, gathers, fallbacks) -> {found, degree sum, gathers, fallbacks}
@@ -1597,7 +1669,8 @@ __global__ void part_bu_counters(const Ctr *c, unsigned long long *out) {
 
 size_t part_bu_scratch_bytes() { return sizeof(Ctl) + 64; }
 
-int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local, int64_t n,
+int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local,
+                   const uint4 *hd_local, int64_t n,
                    int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st) {
@@ -1608,6 +1681,7 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
     A.rs = rs_local - lo;
     A.adj = adj;
     A.posw = posw_local - wlo;
+    A.hd = hd_local - lo;
     A.n = n;
     A.nw = (n + 31) / 32;
     A.arcs = arcs_local;
@@ -1786,6 +1860,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.rs = g->rs.as<OffT>();
     A.adj = g->adj.as<uint32_t>();
     A.posw = g->posw.as<uint32_t>();
+    A.hd = g->hd.as<uint4>();
     A.n = g->n;
     A.nw = g->nw;
     A.arcs = g->arcs;
@@ -1802,8 +1877,6 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     // level arrays that fit L2 take scattered stores cheaply; larger graphs
     // stamp levels once from the depth planes (HBFS_DEFER_LEVELS_MIN_N: test knob)
     A.direct_levels = g->n < env_i64("HBFS_DEFER_LEVELS_MIN_N", int64_t(1) << 22);
-    const bool hubless = g->n > 0 && g->max_degree * g->n < 64 * g->arcs;
-    A.first1_div = env_i64("HBFS_FIRST1_DIV", hubless ? kFirst1Div : 0);  // knob; 0 = never
     A.cbq.q = w->cbq.as<uint32_t>();
     A.cbq.qo = w->cbqo.as<OffT>();
     A.cbq.qr = w->cbqr.as<OffT>();
@@ -1914,7 +1987,8 @@ struct PartTrav {
 static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 2, true, true>; }
 
 void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
-                       const uint32_t *adj, const uint32_t *posw_local, uint32_t *parent_local,
+                       const uint32_t *adj, const uint32_t *posw_local, const uint4 *hd_local,
+                       uint32_t *parent_local,
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad) {
     PartTrav *T = new PartTrav();
     // planes padded to world * (words per rank): the in-place all-gather of a
@@ -1962,6 +2036,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.rs = rs_local - lo;
     A.adj = adj;
     A.posw = posw_local - (lo >> 5);
+    A.hd = hd_local - lo;
     A.n = n;
     A.nw = nw;
     A.arcs = arcs_local;
@@ -1987,7 +2062,6 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
     A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
     A.direct_levels = 1;
-    A.first1_div = 0;
     A.ctl = T->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(T->ctl.as<char>() + sizeof(Ctl));
     A.rows_cap = 1;

@@ -193,6 +193,32 @@ __global__ void k_posw(int64_t n, int64_t nw, const OffT *rs, uint32_t *posw,
     }
 }
 
+// Head records (common.cuh): thread per vertex.
+template <typename OffT>
+__global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, uint4 *hd) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const OffT s = rs[v];
+        const uint64_t d = (uint64_t)(rs[v + 1] - s);
+        uint4 h;
+        h.x = (uint32_t)d;
+        h.y = d > 0 ? adj[(uint64_t)s] : HBFS_NIL;
+        h.z = d > 1 ? adj[(uint64_t)s + 1] : HBFS_NIL;
+        h.w = d > 2 ? adj[(uint64_t)s + 2] : HBFS_NIL;
+        hd[v] = h;
+    }
+}
+
+int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, uint4 *hd, cudaStream_t st) {
+    static_assert(kHeadLen == 3, "head record layout");
+    if (n <= 0) return HBFS_OK;
+    const int blocks = grid_for(n);
+    if (wide) k_heads<uint64_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint64_t *>(rs), adj, hd);
+    else k_heads<uint32_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint32_t *>(rs), adj, hd);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
+}
+
 // Structural check of a caller-supplied CSR (hbfs_graph_from_csr, csr.load of a
 // cache blob): bit 0 row_starts[0] != 0, bit 1 row_starts decreases somewhere,
 // bit 2 an adjacency id >= n.  The traversal kernels index parent/level/bitmaps
@@ -246,6 +272,12 @@ int graph_finalize(hbfs_graph *g, cudaStream_t st) {
     HB_CUDA(cudaStreamSynchronize(st));
     g->max_degree = (int64_t)h;
     cudaGetDevice(&g->device);
+    if (g->max_degree >= (int64_t(1) << 32))
+        return set_error(HBFS_ECAPACITY, "a row of %lld entries exceeds the 32-bit degree of the head records",
+                         (long long)g->max_degree);
+    HB_CHECK(g->hd.alloc((size_t)std::max<int64_t>(g->n, 1) * sizeof(uint4)));
+    HB_CHECK(build_heads(g->n, g->rs.p, g->wide, g->adj.as<uint32_t>(), g->hd.as<uint4>(), st));
+    HB_CUDA(cudaStreamSynchronize(st));
     return HBFS_OK;
 }
 
