@@ -107,7 +107,8 @@ struct Args {
     const OffT *rs;
     const uint32_t *adj;
     const uint32_t *posw;
-    const uint4 *hd;  // head records (common.cuh), indexed like rs
+    const uint4 *hd;      // head records (common.cuh), rank order over the degree > 0 vertices
+    const uint32_t *pre;  // records before bitmap word w (indexed like posw)
     int64_t n, nw, arcs, ncs;
     uint32_t *parent;
     int32_t *level;
@@ -252,21 +253,6 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t *__restrict__ bm, 
 #endif
 }
 
-// Position of the (r+1)-th set bit of m (r < popc(m)); cheaper than __fns.
-__device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t r) {
-    uint32_t pos = 0, c;
-    c = __popc(m & 0xffffu);
-    if (r >= c) { r -= c; m >>= 16; pos += 16; }
-    c = __popc(m & 0xffu);
-    if (r >= c) { r -= c; m >>= 8; pos += 8; }
-    c = __popc(m & 0xfu);
-    if (r >= c) { r -= c; m >>= 4; pos += 4; }
-    c = __popc(m & 0x3u);
-    if (r >= c) { r -= c; m >>= 2; pos += 2; }
-    if (r >= (m & 1u)) pos += 1;
-    return pos;
-}
-
 // Block-aggregated append to a queue: every thread contributes up to I entries
 // (v, deg, row start).  Warps scan their lanes, the CTA scans its warps, and ONE
 // 64-bit atomic per CTA reserves both the queue slots and the arc range
@@ -391,22 +377,34 @@ __device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
     return q;
 }
 
+// Frontier probes of a row vector.  The tests are separated from the plane
+// loads so that the loads stay independent, predicated instructions.
+struct Probe {
+    const uint32_t *bm;  // frontier plane (global-space address, pin_ptr)
+    __device__ __forceinline__ uint32_t word(uint32_t a) const { return probe_word(bm, a); }
+    // 4 entries of a row vector: bit j of the result = val[j] is in the frontier
+    __device__ __forceinline__ uint32_t hits4(const uint32_t (&val)[4], const bool (&ok)[4]) const {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = ok[j] ? word(val[j]) : 0u;
+        uint32_t hm = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hm |= ((w[j] >> (val[j] & 31)) & 1u) << j;
+        return hm;
+    }
+};
+
 // First hit search.  Lane-parallel: for each k, an active lane searches its own
 // sorted row [s, e) for the first entry whose bit is set in `bm`, with aligned
 // uint4 loads (all K rows' loads in flight together).  Lanes unresolved after
 // kLaneVecs vectors are finished by a warp-cooperative scan, 128 entries per
 // step, lowest position winning (ballot + ffs) — the reference's first-hit rule
 // (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
-// FIRST1 (dense frontiers, where nearly every found vertex hits at its first
-// entry): probe that entry alone before the vectors — one bitmap load instead
-// of up to four.
-template <typename OffT, int K, int LV, bool FIRST1, int PF = 0>
-__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
-                                           const uint32_t *__restrict__ bm_in,
+template <typename OffT, int K, int LV, int PF = 0>
+__device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const Probe &bm,
                                            const bool (&act)[K], const OffT (&s)[K],
                                            const OffT (&e)[K], int64_t (&hit)[K],
                                            uint32_t (&hu)[K]) {
-    const uint32_t *__restrict__ bm = pin_ptr(bm_in);
     const int lane = threadIdx.x & 31;
     OffT p[K];
 #pragma unroll
@@ -414,23 +412,6 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
         p[k] = s[k];
         hit[k] = -1;
         hu[k] = 0;
-    }
-    if (FIRST1) {
-        uint32_t a[K], wd[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) a[k] = act[k] && p[k] < e[k] ? __ldg(adj + p[k]) : 0u;
-#pragma unroll
-        for (int k = 0; k < K; ++k) wd[k] = act[k] && p[k] < e[k] ? probe_word(bm, a[k]) : 0u;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (!act[k] || p[k] >= e[k]) continue;
-            if ((wd[k] >> (a[k] & 31)) & 1u) {
-                hit[k] = (int64_t)p[k];
-                hu[k] = a[k];
-            } else {
-                ++p[k];
-            }
-        }
     }
 #pragma unroll
     for (int it = 0; it < LV; ++it) {
@@ -442,7 +423,7 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
             if (go[k]) q4[k] = ld_adj4<PF>(adj + (p[k] & ~(OffT)3));
             else q4[k] = make_uint4(0, 0, 0, 0);
         }
-        uint32_t wd[K][4];
+        bool pok[K][4];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const OffT base = p[k] & ~(OffT)3;
@@ -450,9 +431,15 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const OffT idx = base + j;
-                const bool ok = go[k] && idx >= p[k] && idx < e[k];
-                wd[k][j] = ok ? probe_word(bm, val[j]) : 0u;
+                pok[k][j] = go[k] && idx >= p[k] && idx < e[k];
             }
+        }
+        uint32_t wd[K][4];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wd[k][j] = pok[k][j] ? bm.word(val[j]) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -503,12 +490,10 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                 if (live && b4 < pe) {
                     q4 = __ldg(reinterpret_cast<const uint4 *>(adj + b4));
                     const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
+                    bool ok[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const OffT idx = b4 + j;
-                        if (idx >= ps && idx < pe && ((probe_word(bm, val[j]) >> (val[j] & 31)) & 1u))
-                            hm |= 1u << j;
-                    }
+                    for (int j = 0; j < 4; ++j) ok[j] = b4 + j >= ps && b4 + j < pe;
+                    hm = bm.hits4(val, ok);
                 }
                 const unsigned gm = (__ballot_sync(full, hm != 0) >> (grp * 8)) & 0xffu;
                 const int jm = hm ? __ffs(hm) - 1 : 0;
@@ -548,12 +533,10 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj,
                 if (b4 < pe) {
                     q4 = __ldg(reinterpret_cast<const uint4 *>(adj + b4));
                     const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
+                    bool ok[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint64_t idx = b4 + j;
-                        if (idx >= ps && idx < pe && ((probe_word(bm, val[j]) >> (val[j] & 31)) & 1u))
-                            hm |= 1u << j;
-                    }
+                    for (int j = 0; j < 4; ++j) ok[j] = b4 + j >= ps && b4 + j < pe;
+                    hm = bm.hits4(val, ok);
                 }
                 const unsigned lanes = __ballot_sync(full, hm != 0);
                 if (lanes) {
@@ -966,6 +949,14 @@ struct TileSched {
 
 constexpr int kOpenCap = 64;  // open-list entries per warp: < 32 pending + one push of <= 32
 
+// Bottom-up shared memory (aliases the top-down staging area, idle then).
+// cand: the tile's candidates in vertex order, one 16-bit entry each:
+// (rank of the vertex among its word's degree > 0 bits) << 10 | word << 5 | bit.
+struct BuSmem {
+    uint2 open[kBlock / 32][kOpenCap];
+    uint16_t cand[kBlock / 32][1024];
+};
+
 // Per-thread packed counters of a bottom-up layer:
 // fd = found << 35 | their degree sum; fg = fallbacks << 35 | gathers.
 struct BuCount {
@@ -981,7 +972,7 @@ struct BuCount {
 // Drain up to 32 open candidates (v, degree) from the top of the warp's list:
 // lane i continues row i at position kHeadLen.
 template <typename OffT, int LV, int PF>
-__device__ __forceinline__ void bu_drain(const Args<OffT> &A, const uint32_t *bm_in, uint2 *ol,
+__device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, uint2 *ol,
                                          uint32_t &nopen, int64_t tw, uint32_t *s_found,
                                          int64_t max_pos, int32_t depth1, BuCount &cnt) {
     const int lane = threadIdx.x & 31;
@@ -998,7 +989,7 @@ __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const uint32_t *bm
     const OffT s[1] = {(OffT)(r0 + kHeadLen)}, e[1] = {(OffT)(r0 + ent.y)};
     int64_t hit[1];
     uint32_t hu[1];
-    first_hits<OffT, 1, LV, false, PF>(A.adj, bm_in, act, s, e, hit, hu);
+    first_hits<OffT, 1, LV, PF>(A.adj, bm, act, s, e, hit, hu);
     if (act[0]) {
         const bool found = hit[0] >= 0;
         if (found) {
@@ -1018,7 +1009,9 @@ __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const uint32_t *bm
 template <typename OffT, int C, int LV, bool PART = false, int PF = 0>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found,
-                         uint2 *ol) {
+                         BuSmem &bs) {
+    uint2 *ol = bs.open[threadIdx.x >> 5];
+    uint16_t *cl = bs.cand[threadIdx.x >> 5];
     const unsigned full = 0xffffffffu;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -1027,7 +1020,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     const Plane vis{A.bits};
     const int64_t max_pos = A.max_pos;
     const int32_t depth1 = (int32_t)S.layer + 1;
-    const uint32_t *__restrict__ bm = pin_ptr(in.p);
+    const Probe bm{pin_ptr(in.p)};
     BuCount cnt;
     const int64_t w0 = PART ? A.part_w0 : 0, wend = PART ? A.part_wend : A.nw;
     const int64_t ntiles = (wend - w0 + 31) >> 5;
@@ -1040,6 +1033,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         const uint32_t vis0 = valid ? vis[wl] : ~0u;
         const uint32_t inl = valid ? in[wl] : 0u;
         const uint32_t pwl = valid ? __ldg(A.posw + wl) : 0u;
+        const uint32_t prel = valid ? __ldg(A.pre + wl) : 0u;
         if (!PART && valid) clear_spare_word(A, S.layer, wl);
         const uint32_t vwl = vis0 | inl;
         const uint32_t candl = ~vwl & pwl;
@@ -1054,6 +1048,14 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         const uint32_t T = __shfl_sync(full, incl, 31);
         if (T == 0) continue;
         s_found[lane] = 0;
+        // the lane lists its word's candidates at their positions in tile order
+        {
+            uint32_t pos = incl - cntl;
+            for (uint32_t m = candl; m; m &= m - 1) {
+                const uint32_t bit = __ffs(m) - 1;
+                cl[pos++] = (uint16_t)(__popc(pwl & ((1u << bit) - 1u)) << 10 | lane << 5 | bit);
+            }
+        }
         __syncwarp();
         uint32_t nopen = 0;  // warp-uniform
         for (uint32_t b = 0; b < T; b += 32 * C) {
@@ -1064,21 +1066,14 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             for (int k = 0; k < C; ++k) {
                 const uint32_t c = b + k * 32 + lane;
                 act[k] = c < T;
-                int j = 0;  // word holding candidate c: lanes with incl <= c
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const uint32_t val = __shfl_sync(full, incl, j + step - 1);
-                    if (val <= c) j += step;
-                }
-                if (j > 31) j = 31;
-                const uint32_t cm = __shfl_sync(full, candl, j);
-                const uint32_t ex = __shfl_sync(full, incl, j) - __shfl_sync(full, cntl, j);
-                const uint32_t bit = act[k] ? nth_bit(cm, c - ex) : 0u;
-                v[k] = (uint32_t)((tw + j) * 32 + bit);
+                const uint32_t ent = act[k] ? cl[c] : 0u;
+                v[k] = (uint32_t)(tw * 32) + (ent & 1023u);
+                // record slot: rank of v among the degree > 0 vertices
+                const uint32_t slot = __shfl_sync(full, prel, (ent >> 5) & 31) + (ent >> 10);
                 h[k] = make_uint4(0u, 0u, 0u, 0u);
                 if (act[k]) {
                     HB_DCHECK(v[k] < A.n, 6);
-                    h[k] = __ldg(A.hd + v[k]);
+                    h[k] = __ldg(A.hd + slot);
                 }
             }
             // Probes in two steps: the first head entry alone (it decides most
@@ -1088,12 +1083,12 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             uint32_t pw[C][kHeadLen];
 #pragma unroll
             for (int k = 0; k < C; ++k)  // degree 0 when inactive: no probe
-                pw[k][0] = h[k].x > 0 ? probe_word(bm, h[k].y) : 0u;
+                pw[k][0] = h[k].x > 0 ? bm.word(h[k].y) : 0u;
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const bool more = !((pw[k][0] >> (h[k].y & 31)) & 1u);
-                pw[k][1] = more && h[k].x > 1 ? probe_word(bm, h[k].z) : 0u;
-                pw[k][2] = more && h[k].x > 2 ? probe_word(bm, h[k].w) : 0u;
+                pw[k][1] = more && h[k].x > 1 ? bm.word(h[k].z) : 0u;
+                pw[k][2] = more && h[k].x > 2 ? bm.word(h[k].w) : 0u;
             }
 #pragma unroll
             for (int k = 0; k < C; ++k) {
@@ -1119,11 +1114,11 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                     nopen += __popc(m);
                     __syncwarp();
                     if (nopen >= 32u)
-                        bu_drain<OffT, LV, PF>(A, in.p, ol, nopen, tw, s_found, max_pos, depth1, cnt);
+                        bu_drain<OffT, LV, PF>(A, bm, ol, nopen, tw, s_found, max_pos, depth1, cnt);
                 }
             }
         }
-        while (nopen) bu_drain<OffT, LV, PF>(A, in.p, ol, nopen, tw, s_found, max_pos, depth1, cnt);
+        while (nopen) bu_drain<OffT, LV, PF>(A, bm, ol, nopen, tw, s_found, max_pos, depth1, cnt);
         __syncwarp();
         const uint32_t f = s_found[lane];
         if (valid && f) {
@@ -1583,11 +1578,11 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                     if (x && (vis_all[w] & x) != x) vis_all[w] |= x;
                 }
             }
-            uint2 *ol = reinterpret_cast<uint2 *>(dsm) + (threadIdx.x >> 5) * kOpenCap;  // TdSmem is idle
-            if (SCAN && S.v_f * 64 < A.n)  // tiny frontier: open rows are mostly scanned to their end
-                phase_bu<OffT, K, kLaneVecsScan, PART>(A, S, in, out, spare, ctr, red, sf, ol);
+            BuSmem &bs = *reinterpret_cast<BuSmem *>(dsm);  // the top-down staging area is idle
+            if (SCAN && S.v_f * 64 < A.n)  // small frontier: open rows are mostly scanned to their end
+                phase_bu<OffT, K, kLaneVecsScan, PART>(A, S, in, out, spare, ctr, red, sf, bs);
             else
-                phase_bu<OffT, K, kLaneVecs, PART>(A, S, in, out, spare, ctr, red, sf, ol);
+                phase_bu<OffT, K, kLaneVecs, PART>(A, S, in, out, spare, ctr, red, sf, bs);
         }
         grid.sync();
 
@@ -1654,9 +1649,9 @@ __global__ void __launch_bounds__(kBlock, 2) part_bu_kernel(Args<OffT> A, St S, 
                                                           uint32_t *outp) {
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];
-    __shared__ uint2 s_open[(kBlock / 32) * kOpenCap];
+    __shared__ BuSmem bs;
     phase_bu<OffT, K, LV, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
-                                ctr, red, s_found + (threadIdx.x & ~31), s_open + (threadIdx.x >> 5) * kOpenCap);
+                                ctr, red, s_found + (threadIdx.x & ~31), bs);
 }
 
 // Ctr (found << 35 | degree sum, gathers, fallbacks) -> {found, degree sum, gathers, fallbacks}
@@ -1670,7 +1665,7 @@ __global__ void part_bu_counters(const Ctr *c, unsigned long long *out) {
 size_t part_bu_scratch_bytes() { return sizeof(Ctl) + 64; }
 
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local,
-                   const uint4 *hd_local, int64_t n,
+                   const uint4 *hd_local, const uint32_t *pre_local, int64_t n,
                    int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st) {
@@ -1681,7 +1676,8 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
     A.rs = rs_local - lo;
     A.adj = adj;
     A.posw = posw_local - wlo;
-    A.hd = hd_local - lo;
+    A.hd = hd_local;  // rank order within the partition
+    A.pre = pre_local - (lo >> 5);
     A.n = n;
     A.nw = (n + 31) / 32;
     A.arcs = arcs_local;
@@ -1745,10 +1741,6 @@ constexpr int kDefaultVariant = 0;
 // Measured on B200 (tools/diag.py sweeps): small graphs are latency-bound and
 // prefer one fat CTA per SM with 4 searches in flight per lane (variant 4);
 // SCALE >= 24 prefers two CTAs per SM with 2 searches per lane (variant 3).
-static int64_t env_i64(const char *name, int64_t dflt) {
-    const char *e = getenv(name);
-    return e ? atoll(e) : dflt;
-}
 
 static int variant_index(int64_t n) {
     const char *e = getenv("HBFS_KERNEL_VARIANT");
@@ -1778,11 +1770,18 @@ struct Workspace {
     }
 };
 
+static int64_t env_i64(const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    return e ? atoll(e) : dflt;
+}
+
 template <typename OffT>
 static size_t dyn_smem_bytes() {
-    size_t b = sizeof(TdSmem<OffT>);
+    size_t b = sizeof(TdSmem<OffT>);  // top-down phases; bottom-up: open lists + candidate lists
+    if (sizeof(BuSmem) > b) b = sizeof(BuSmem);
     return (b + 15) & ~(size_t)15;
 }
+
 
 static size_t ctl_bytes() { return sizeof(Ctl) + kRowsCap * sizeof(hbfs_layer_row); }
 
@@ -1861,6 +1860,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.adj = g->adj.as<uint32_t>();
     A.posw = g->posw.as<uint32_t>();
     A.hd = g->hd.as<uint4>();
+    A.pre = g->pre.as<uint32_t>();
     A.n = g->n;
     A.nw = g->nw;
     A.arcs = g->arcs;
@@ -1988,7 +1988,7 @@ static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 
 
 void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
                        const uint32_t *adj, const uint32_t *posw_local, const uint4 *hd_local,
-                       uint32_t *parent_local,
+                       const uint32_t *pre_local, uint32_t *parent_local,
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad) {
     PartTrav *T = new PartTrav();
     // planes padded to world * (words per rank): the in-place all-gather of a
@@ -2036,7 +2036,8 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.rs = rs_local - lo;
     A.adj = adj;
     A.posw = posw_local - (lo >> 5);
-    A.hd = hd_local - lo;
+    A.hd = hd_local;  // rank order within the partition
+    A.pre = pre_local - (lo >> 5);
     A.n = n;
     A.nw = nw;
     A.arcs = arcs_local;

@@ -142,16 +142,20 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
 // resolve most candidates from this record alone — first hit among the head
 // entries, or a row that ends inside the head — without touching the row
 // starts or the adjacency array; only rows still open continue at position
-// kHeadLen of the CSR row.  Built once per graph (graph_finalize / part build).
+// kHeadLen of the CSR row.  The records are packed in rank order over the
+// vertices with degree > 0 (`pre[w]` = records before bitmap word w), so the
+// candidates of a dense layer read them as contiguous runs.  Built once per
+// graph (graph_finalize / part build); synchronises the stream.
 constexpr int kHeadLen = 3;
-int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, uint4 *hd, cudaStream_t st);
+int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
+                DevBuf &pre, DevBuf &hd, cudaStream_t st);
 
 // Bottom-up layer of one partition rank with the persistent kernel's tile
 // machinery (defined in bfs.cu, used by part.cu).  v_f: global frontier size
 // (< 0: unknown).  scratch: part_bu_scratch_bytes() of device memory.
 size_t part_bu_scratch_bytes();
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local,
-                   const uint4 *hd_local, int64_t n,
+                   const uint4 *hd_local, const uint32_t *pre_local, int64_t n,
                    int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st);
@@ -160,7 +164,7 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
 // (bfs.cu; driven by the multi-GPU loop in part.cu).
 void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
                        const uint32_t *adj, const uint32_t *posw_local, const uint4 *hd_local,
-                       uint32_t *parent_local,
+                       const uint32_t *pre_local, uint32_t *parent_local,
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad);
 void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
@@ -181,7 +185,8 @@ struct hbfs_graph {
     hbfs::DevBuf rs;       // OffT[n+1]
     hbfs::DevBuf adj;      // uint32[arcs + 8] (padded for aligned uint4 reads)
     hbfs::DevBuf posw;     // uint32[nw]: bit v = deg(v) > 0 (engine.py:29-57 `posw`)
-    hbfs::DevBuf hd;       // uint4[n] head records: {deg, row[0], row[1], row[2]} (absent = NIL)
+    hbfs::DevBuf hd;       // uint4[#deg>0] head records: {deg, row[0], row[1], row[2]} (absent = NIL)
+    hbfs::DevBuf pre;      // uint32[nw+1]: head records before bitmap word w
     hbfs::Workspace *ws = nullptr;
     // hbfs_bfs holds this for the whole call: the per-graph workspace (parent,
     // level, bitmaps, queues, controller state, pinned trace mirror) serves one

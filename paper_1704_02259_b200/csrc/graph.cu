@@ -193,29 +193,65 @@ __global__ void k_posw(int64_t n, int64_t nw, const OffT *rs, uint32_t *posw,
     }
 }
 
-// Head records (common.cuh): thread per vertex.
+// Head records (common.cuh), packed in rank order over the vertices with
+// degree > 0: pre[w] = number of such vertices before bitmap word w, so vertex
+// v = 32 w + b sits at pre[w] + popc(posw[w] & ((1 << b) - 1)).
+struct PopcOp {
+    __host__ __device__ uint32_t operator()(uint32_t x) const {
+#ifdef __CUDA_ARCH__
+        return __popc(x);
+#else
+        return (uint32_t)__builtin_popcount(x);
+#endif
+    }
+};
+
 template <typename OffT>
-__global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, uint4 *hd) {
+__global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, const uint32_t *posw,
+                        const uint32_t *pre, uint4 *hd) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         const OffT s = rs[v];
         const uint64_t d = (uint64_t)(rs[v + 1] - s);
+        if (d == 0) continue;
         uint4 h;
         h.x = (uint32_t)d;
-        h.y = d > 0 ? adj[(uint64_t)s] : HBFS_NIL;
+        h.y = adj[(uint64_t)s];
         h.z = d > 1 ? adj[(uint64_t)s + 1] : HBFS_NIL;
         h.w = d > 2 ? adj[(uint64_t)s + 2] : HBFS_NIL;
-        hd[v] = h;
+        hd[pre[v >> 5] + __popc(posw[v >> 5] & ((1u << (v & 31)) - 1u))] = h;
     }
 }
 
-int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, uint4 *hd, cudaStream_t st) {
+int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
+                DevBuf &pre, DevBuf &hd, cudaStream_t st) {
     static_assert(kHeadLen == 3, "head record layout");
+    const int64_t nw = (n + 31) / 32;
+    HB_CHECK(pre.alloc((nw + 1) * 4 + 16));
+    uint32_t total = 0;
+    if (nw > 0) {
+        // exclusive scan over nw + 1 items: pre[nw] = number of records (posw
+        // is allocated with slack, the value read at nw does not matter)
+        cub::TransformInputIterator<uint32_t, PopcOp, const uint32_t *> in(posw, PopcOp());
+        size_t tb = 0;
+        HB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, pre.as<uint32_t>(), nw + 1, st));
+        DevBuf tmp;
+        HB_CHECK(tmp.alloc(tb));
+        HB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, pre.as<uint32_t>(), nw + 1, st));
+        HB_CUDA(cudaMemcpyAsync(&total, pre.as<uint32_t>() + nw, 4, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+    }
+    HB_CHECK(hd.alloc(((size_t)total + 1) * sizeof(uint4)));
     if (n <= 0) return HBFS_OK;
     const int blocks = grid_for(n);
-    if (wide) k_heads<uint64_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint64_t *>(rs), adj, hd);
-    else k_heads<uint32_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint32_t *>(rs), adj, hd);
+    if (wide)
+        k_heads<uint64_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint64_t *>(rs), adj, posw,
+                                                 pre.as<uint32_t>(), hd.as<uint4>());
+    else
+        k_heads<uint32_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint32_t *>(rs), adj, posw,
+                                                 pre.as<uint32_t>(), hd.as<uint4>());
     HB_CUDA(cudaGetLastError());
+    HB_CUDA(cudaStreamSynchronize(st));
     return HBFS_OK;
 }
 
@@ -275,9 +311,7 @@ int graph_finalize(hbfs_graph *g, cudaStream_t st) {
     if (g->max_degree >= (int64_t(1) << 32))
         return set_error(HBFS_ECAPACITY, "a row of %lld entries exceeds the 32-bit degree of the head records",
                          (long long)g->max_degree);
-    HB_CHECK(g->hd.alloc((size_t)std::max<int64_t>(g->n, 1) * sizeof(uint4)));
-    HB_CHECK(build_heads(g->n, g->rs.p, g->wide, g->adj.as<uint32_t>(), g->hd.as<uint4>(), st));
-    HB_CUDA(cudaStreamSynchronize(st));
+    HB_CHECK(build_heads(g->n, g->rs.p, g->wide, g->adj.as<uint32_t>(), g->posw.as<uint32_t>(), g->pre, g->hd, st));
     return HBFS_OK;
 }
 

@@ -44,7 +44,7 @@ struct Part {
     int ranges = 1;
     DevBuf scratch;           // counters etc.
     DevBuf posw;              // uint32[wloc] deg > 0 bits of the owned vertices
-    DevBuf hd;                // uint4[nloc] head records of the owned rows (common.cuh)
+    DevBuf hd, pre;           // head records of the owned rows, rank order + per-word prefix (common.cuh)
     DevBuf bu_scratch;        // part_bu_launch scratch (Ctl)
     int64_t fhint = -1;       // global frontier size of the next bottom-up layer (-1: unknown)
     // top-down exchange state (all kept clean between layers)
@@ -425,8 +425,7 @@ static int part_alloc_state(Part *P) {
     HB_CHECK(P->bu_scratch.alloc(part_bu_scratch_bytes()));
     HB_CUDA(cudaDeviceSynchronize());  // rs was built on the caller's stream
     kp_posw<<<pgrid(P->wloc), 256>>>(P->nloc, P->wloc, P->rs.as<uint64_t>(), P->posw.as<uint32_t>());
-    HB_CHECK(P->hd.alloc((size_t)std::max<int64_t>(P->nloc, 1) * sizeof(uint4)));
-    HB_CHECK(build_heads(P->nloc, P->rs.p, 1, P->adj.as<uint32_t>(), P->hd.as<uint4>(), 0));
+    HB_CHECK(build_heads(P->nloc, P->rs.p, 1, P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->pre, P->hd, 0));
     {
         const int64_t nseg = P->arcs / kSegArcs + P->nloc / 1024 + 16;
         HB_CHECK(P->seg_u.alloc(nseg * 4));
@@ -655,7 +654,7 @@ extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32
     if (!P || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the persistent kernel's bottom-up tiles on the owned words (bfs.cu)
-    HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->n, P->lo,
+    HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->pre.as<uint32_t>(), P->n, P->lo,
                             P->nloc, P->arcs, P->F.as<uint32_t>(), P->V.as<uint32_t>(), P->parent.as<uint32_t>(),
                             P->level.as<int32_t>(), next_slice, depth, max_pos, P->fhint, counters,
                             P->bu_scratch.p, st));
@@ -939,7 +938,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
         if (!P->trav) {
             int rc = HBFS_OK;
             P->trav = part_trav_create(n, P->lo, P->nloc, P->arcs, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-                                       P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->parent.as<uint32_t>(),
+                                       P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->pre.as<uint32_t>(), P->parent.as<uint32_t>(),
                                        P->level.as<int32_t>(),
                                        reinterpret_cast<uint32_t *>(P->cand.as<int32_t>()), P->touch.as<uint32_t>(),
                                        &rc, nw_pad);

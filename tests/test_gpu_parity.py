@@ -84,9 +84,6 @@ KNOBS = {
     "defer": {"HBFS_DEFER_LEVELS_MIN_N": "0"},
     # the large-graph kernel variant (2 searches/lane, scan-tuned bottom-up)
     "scan_variant": {"HBFS_KERNEL_VARIANT": "3"},
-    # single first-entry probe on every bottom-up layer (normally hubless graphs,
-    # frontier >= n/16)
-    "first1": {"HBFS_FIRST1_DIV": str(1 << 30)},
 }
 
 
