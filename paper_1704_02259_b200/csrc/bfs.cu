@@ -931,18 +931,25 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
 // gathers/fallbacks are those of the reference's 16-lane kernel.
 // Replaces bottom_up_multiple_set / bottom_up_layer (_native.pyx:89-204,
 // bu_probe.h:22-106).
-// Warp tile scheduler: the first tile is the warp's own index (no atomic, so
-// short layers spread over all warps), then one tile per atomic grab from a
-// per-layer counter (balances long layers).
+// Warp tile scheduler: a warp first walks its own strided share of the leading
+// kStaticNum/kStaticDen of the tiles (no atomics: a layer whose tiles are
+// mostly empty would otherwise spend its time on one contended counter), then
+// draws the remaining tiles one per atomic grab (balances the end of long
+// layers).
+constexpr int64_t kStaticNum = 7, kStaticDen = 8;
 struct TileSched {
     unsigned long long *work;
-    int64_t tile, nwarps;
-    __device__ TileSched(unsigned long long *w, int64_t warp, int64_t nw)
-        : work(w), tile(warp), nwarps(nw) {}
+    int64_t tile, nwarps, nstatic;  // nstatic: tiles handed out statically
+    __device__ TileSched(unsigned long long *w, int64_t warp, int64_t nw, int64_t ntiles)
+        : work(w), tile(warp), nwarps(nw) {
+        const int64_t rounds = ntiles * kStaticNum / kStaticDen / nw;
+        nstatic = (rounds > 0 ? rounds : 1) * nw;
+    }
     __device__ __forceinline__ int64_t next() {
+        if (tile + nwarps < nstatic) return tile += nwarps;
         unsigned long long t = 0;
         if ((threadIdx.x & 31) == 0) t = atomicAdd(work, 1ull);
-        tile = nwarps + (int64_t)__shfl_sync(0xffffffffu, t, 0);
+        tile = nstatic + (int64_t)__shfl_sync(0xffffffffu, t, 0);
         return tile;
     }
 };
@@ -1025,7 +1032,7 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
     const int64_t w0 = PART ? A.part_w0 : 0, wend = PART ? A.part_wend : A.nw;
     const int64_t ntiles = (wend - w0 + 31) >> 5;
 
-    TileSched ts(&A.ctl->work[S.layer % 3], tid >> 5, nth >> 5);
+    TileSched ts(&A.ctl->work[S.layer % 3], tid >> 5, nth >> 5, ntiles);
     for (int64_t tile = ts.tile; tile < ntiles; tile = ts.next()) {
         const int64_t tw = w0 + tile * 32;  // first word of the tile
         const int64_t wl = tw + lane;
