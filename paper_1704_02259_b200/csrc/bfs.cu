@@ -394,94 +394,69 @@ struct Probe {
     }
 };
 
-// First hit search.  Lane-parallel: for each k, an active lane searches its own
-// sorted row [s, e) for the first entry whose bit is set in `bm`, with aligned
-// uint4 loads (all K rows' loads in flight together).  Lanes unresolved after
-// kLaneVecs vectors are finished by a warp-cooperative scan, 128 entries per
-// step, lowest position winning (ballot + ffs) — the reference's first-hit rule
-// (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
-template <typename OffT, int K, int LV, int PF = 0>
+// First hit search of up to 32 rows, one per lane: the first entry of the
+// sorted row [s, e) whose bit is set in the frontier plane — the reference's
+// first-hit rule (_native.pyx:98-104, bu_probe.h:38-63 + fallback :186-203).
+// Each lane first walks its own row for up to `lv` aligned uint4 vectors;
+// rows still open are finished cooperatively, lowest position winning (ballot
+// + ffs): four rows at a time by 8-lane groups (32 entries per row and step),
+// rows with more than kTailLong entries left by the whole warp (128 entries
+// per step).  The loops are deliberately not unrolled and the two cooperative
+// widths share one body: the bottom-up hot path has to stay inside the 32 KB
+// instruction cache (ncu: `no_instruction` stalls dominated a larger variant).
+template <typename OffT, int PF = 0>
 __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, const Probe &bm,
-                                           const bool (&act)[K], const OffT (&s)[K],
-                                           const OffT (&e)[K], int64_t (&hit)[K],
-                                           uint32_t (&hu)[K]) {
+                                           const bool act, const OffT s, const OffT e, int lv,
+                                           int64_t &hit, uint32_t &hu) {
+    const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    OffT p[K];
+    OffT p = s;
+    hit = -1;
+    hu = 0;
+#pragma unroll 1
+    for (int it = 0; it < lv; ++it) {
+        const bool go = act && hit < 0 && p < e;
+        if (!__any_sync(full, go)) break;
+        const OffT base = p & ~(OffT)3;
+        uint4 q4 = make_uint4(0, 0, 0, 0);
+        if (go) q4 = ld_adj4<PF>(adj + base);
+        const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
+        bool ok[4];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        p[k] = s[k];
-        hit[k] = -1;
-        hu[k] = 0;
-    }
-#pragma unroll
-    for (int it = 0; it < LV; ++it) {
-        uint4 q4[K];
-        bool go[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            go[k] = act[k] && hit[k] < 0 && p[k] < e[k];
-            if (go[k]) q4[k] = ld_adj4<PF>(adj + (p[k] & ~(OffT)3));
-            else q4[k] = make_uint4(0, 0, 0, 0);
-        }
-        bool pok[K][4];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const OffT base = p[k] & ~(OffT)3;
-            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const OffT idx = base + j;
-                pok[k][j] = go[k] && idx >= p[k] && idx < e[k];
-            }
-        }
-        uint32_t wd[K][4];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) wd[k][j] = pok[k][j] ? bm.word(val[j]) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (!go[k]) continue;
-            const OffT base = p[k] & ~(OffT)3;
-            const uint32_t val[4] = {q4[k].x, q4[k].y, q4[k].z, q4[k].w};
-            uint32_t hm = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) hm |= ((wd[k][j] >> (val[j] & 31)) & 1u) << j;
-            // wd is 0 for out-of-row entries, so a set bit is always in range
+        for (int j = 0; j < 4; ++j) ok[j] = go && base + j >= p && base + j < e;
+        const uint32_t hm = bm.hits4(val, ok);
+        if (go) {
             if (hm) {
                 const int j = __ffs(hm) - 1;
-                hit[k] = (int64_t)(base + j);
+                hit = (int64_t)(base + j);
                 // select, not val[j]: a dynamic index would put val[] in local memory
-                hu[k] = j == 0 ? val[0] : j == 1 ? val[1] : j == 2 ? val[2] : val[3];
+                hu = j == 0 ? val[0] : j == 1 ? val[1] : j == 2 ? val[2] : val[3];
             } else {
-                p[k] = base + 4;
+                p = base + 4;
             }
         }
     }
-    // Rows still open: short ones four at a time (8 lanes x 4 entries per row
-    // per step, lowest position in each 8-lane group wins), rows with more than
-    // kTailLong entries left by the whole warp (128 entries per step).
-    const unsigned full = 0xffffffffu;
-    const int grp = lane >> 3, gl = lane & 7;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const bool open = act[k] && hit[k] < 0 && p[k] < e[k];
-        unsigned todo_long = __ballot_sync(full, open && (uint64_t)(e[k] - p[k]) > kTailLong);
-        unsigned todo = __ballot_sync(full, open) & ~todo_long;
+    const bool open = act && hit < 0 && p < e;
+    const unsigned todo_long = __ballot_sync(full, open && (uint64_t)(e - p) > kTailLong);
+    const unsigned todo_short = __ballot_sync(full, open) & ~todo_long;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        unsigned todo = pass ? todo_long : todo_short;
+        const int gsh = pass ? 5 : 3;                  // lanes per row: 8, then 32
+        const int gw = 1 << gsh, grp = lane >> gsh, gl = lane & (gw - 1), ng = 32 >> gsh;
+        const unsigned gmask = gw == 32 ? ~0u : (1u << gw) - 1u;
         while (todo) {
             unsigned t = todo;
             for (int g = 0; g < grp && t; ++g) t &= t - 1;  // group g takes the g-th open row
             const int src = t ? __ffs(t) - 1 : -1;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) todo &= todo - 1;
+            for (int g = 0; g < ng; ++g) todo &= todo - 1;
             const int sl = src < 0 ? 0 : src;
-            const OffT ps = __shfl_sync(full, p[k], sl), pe = __shfl_sync(full, e[k], sl);
+            const OffT ps = __shfl_sync(full, p, sl), pe = __shfl_sync(full, e, sl);
             bool live = src >= 0;
             int64_t h = -1;
             uint32_t hv = 0;
-            for (OffT c = ps & ~(OffT)3;; c += 32) {
+#pragma unroll 1
+            for (OffT c = ps & ~(OffT)3;; c += 4 * gw) {
                 live = live && c < pe;
                 if (!__any_sync(full, live)) break;
                 const OffT b4 = c + 4 * gl;
@@ -495,11 +470,11 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
                     for (int j = 0; j < 4; ++j) ok[j] = b4 + j >= ps && b4 + j < pe;
                     hm = bm.hits4(val, ok);
                 }
-                const unsigned gm = (__ballot_sync(full, hm != 0) >> (grp * 8)) & 0xffu;
+                const unsigned gm = (__ballot_sync(full, hm != 0) >> (grp << gsh)) & gmask;
                 const int jm = hm ? __ffs(hm) - 1 : 0;
                 const uint32_t mine = jm == 0 ? q4.x : jm == 1 ? q4.y : jm == 2 ? q4.z : q4.w;
                 const int wl = gm ? __ffs(gm) - 1 : 0;
-                const int srcl = grp * 8 + wl;
+                const int srcl = (grp << gsh) + wl;
                 const int jw = __shfl_sync(full, jm, srcl);
                 const uint32_t vw = __shfl_sync(full, mine, srcl);
                 if (live && gm) {
@@ -508,49 +483,15 @@ __device__ __forceinline__ void first_hits(const uint32_t *__restrict__ adj, con
                     live = false;
                 }
             }
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {  // results back to the rows' owners
-                const int og = __shfl_sync(full, src, g * 8);
-                const int64_t hg = __shfl_sync(full, (long long)h, g * 8);
-                const uint32_t vg = __shfl_sync(full, hv, g * 8);
+#pragma unroll 1
+            for (int g = 0; g < ng; ++g) {  // results back to the rows' owners
+                const int og = __shfl_sync(full, src, g << gsh);
+                const int64_t hg = __shfl_sync(full, (long long)h, g << gsh);
+                const uint32_t vg = __shfl_sync(full, hv, g << gsh);
                 if (lane == og) {
-                    hit[k] = hg;
-                    hu[k] = vg;
+                    hit = hg;
+                    hu = vg;
                 }
-            }
-        }
-        while (todo_long) {
-            const int src = __ffs(todo_long) - 1;
-            todo_long &= todo_long - 1;
-            const uint64_t ps = __shfl_sync(full, (unsigned long long)p[k], src);
-            const uint64_t pe = __shfl_sync(full, (unsigned long long)e[k], src);
-            int64_t h = -1;
-            uint32_t hv = 0;
-            for (uint64_t c = ps & ~3ull; c < pe; c += 128) {
-                const uint64_t b4 = c + 4 * lane;
-                uint32_t hm = 0;
-                uint4 q4 = make_uint4(0, 0, 0, 0);
-                if (b4 < pe) {
-                    q4 = __ldg(reinterpret_cast<const uint4 *>(adj + b4));
-                    const uint32_t val[4] = {q4.x, q4.y, q4.z, q4.w};
-                    bool ok[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) ok[j] = b4 + j >= ps && b4 + j < pe;
-                    hm = bm.hits4(val, ok);
-                }
-                const unsigned lanes = __ballot_sync(full, hm != 0);
-                if (lanes) {
-                    const int l = __ffs(lanes) - 1;
-                    const int j = __ffs(__shfl_sync(full, hm, l)) - 1;
-                    const uint32_t mine = j == 0 ? q4.x : j == 1 ? q4.y : j == 2 ? q4.z : q4.w;
-                    hv = __shfl_sync(full, mine, l);
-                    h = (int64_t)(c + 4 * l + j);
-                    break;
-                }
-            }
-            if (lane == src) {
-                hit[k] = h;
-                hu[k] = hv;
             }
         }
     }
@@ -954,13 +895,14 @@ struct TileSched {
     }
 };
 
-constexpr int kOpenCap = 64;  // open-list entries per warp: < 32 pending + one push of <= 32
+constexpr int kOpenCap = 160;  // open-list entries per warp: < 32 pending + one round's pushes (<= 32 * 4)
 
 // Bottom-up shared memory (aliases the top-down staging area, idle then).
 // cand: the tile's candidates in vertex order, one 16-bit entry each:
 // (rank of the vertex among its word's degree > 0 bits) << 10 | word << 5 | bit.
+// open: candidates their head record did not resolve, same entries.
 struct BuSmem {
-    uint2 open[kBlock / 32][kOpenCap];
+    uint16_t open[kBlock / 32][kOpenCap];
     uint16_t cand[kBlock / 32][1024];
 };
 
@@ -976,36 +918,40 @@ struct BuCount {
     }
 };
 
-// Drain up to 32 open candidates (v, degree) from the top of the warp's list:
-// lane i continues row i at position kHeadLen.
-template <typename OffT, int LV, int PF>
-__device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, uint2 *ol,
-                                         uint32_t &nopen, int64_t tw, uint32_t *s_found,
-                                         int64_t max_pos, int32_t depth1, BuCount &cnt) {
+// Drain up to 32 open candidates from the top of the warp's list: lane i
+// continues row i at position kHeadLen (its degree is re-read from the head
+// record, a cache hit).
+template <typename OffT, int PF>
+__device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, const uint16_t *ol,
+                                         uint32_t &nopen, int64_t tw, uint32_t prel, uint32_t *s_found,
+                                         int64_t max_pos, int32_t depth1, int lv, BuCount &cnt) {
     const int lane = threadIdx.x & 31;
     const uint32_t take = nopen < 32u ? nopen : 32u;
     nopen -= take;
-    const bool act[1] = {(uint32_t)lane < take};
-    const uint2 ent = act[0] ? ol[nopen + lane] : make_uint2(0u, 0u);
+    const bool act = (uint32_t)lane < take;
+    const uint32_t oe = act ? ol[nopen + lane] : 0u;
+    const uint32_t slot = __shfl_sync(0xffffffffu, prel, (oe >> 5) & 31) + (oe >> 10);
+    uint2 ent = make_uint2((uint32_t)(tw * 32) + (oe & 1023u), 0u);  // vertex, degree
     OffT r0 = 0;
-    if (act[0]) {
+    if (act) {
+        ent.y = __ldg(&A.hd[slot].x);
         HB_DCHECK(ent.x < A.n, 6);
         r0 = __ldg(A.rs + ent.x);
         HB_DCHECK((int64_t)r0 + ent.y <= A.arcs, 4);
     }
-    const OffT s[1] = {(OffT)(r0 + kHeadLen)}, e[1] = {(OffT)(r0 + ent.y)};
-    int64_t hit[1];
-    uint32_t hu[1];
-    first_hits<OffT, 1, LV, PF>(A.adj, bm, act, s, e, hit, hu);
-    if (act[0]) {
-        const bool found = hit[0] >= 0;
+    const OffT s = (OffT)(r0 + kHeadLen), e = (OffT)(r0 + ent.y);
+    int64_t hit;
+    uint32_t hu;
+    first_hits<OffT, PF>(A.adj, bm, act, s, e, lv, hit, hu);
+    if (act) {
+        const bool found = hit >= 0;
         if (found) {
-            HB_DCHECK(hu[0] < A.n && hit[0] < (int64_t)e[0] && hit[0] >= (int64_t)s[0], 0);
-            A.parent[ent.x] = hu[0];
+            HB_DCHECK(hu < A.n && hit < (int64_t)e && hit >= (int64_t)s, 0);
+            A.parent[ent.x] = hu;
             if (A.direct_levels) A.level[ent.x] = depth1;
             atomicOr(&s_found[(ent.x >> 5) - tw], 1u << (ent.x & 31));
         }
-        cnt.add(found, found ? hit[0] - (int64_t)r0 : -1, (int64_t)ent.y, max_pos);
+        cnt.add(found, found ? hit - (int64_t)r0 : -1, (int64_t)ent.y, max_pos);
     }
     __syncwarp();  // the list slots just read may be pushed over
 }
@@ -1013,11 +959,11 @@ __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, u
 // PART: one rank's share of a 1D partition (csrc/part.cu): tiles cover the
 // owned words [part_w0, part_wend) only; the arrays indexed by vertex or word
 // are offset pointers (see part_bu_launch), and there is no depth ring.
-template <typename OffT, int C, int LV, bool PART = false, int PF = 0>
+template <typename OffT, int C, bool PART = false, int PF = 0>
 __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
                          const Plane spare, Ctr *ctr, unsigned long long *red, uint32_t *s_found,
-                         BuSmem &bs) {
-    uint2 *ol = bs.open[threadIdx.x >> 5];
+                         BuSmem &bs, int lv) {
+    uint16_t *ol = bs.open[threadIdx.x >> 5];
     uint16_t *cl = bs.cand[threadIdx.x >> 5];
     const unsigned full = 0xffffffffu;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1067,13 +1013,13 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
         uint32_t nopen = 0;  // warp-uniform
         for (uint32_t b = 0; b < T; b += 32 * C) {
             bool act[C];
-            uint32_t v[C];
+            uint32_t v[C], ce[C];
             uint4 h[C];
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const uint32_t c = b + k * 32 + lane;
                 act[k] = c < T;
-                const uint32_t ent = act[k] ? cl[c] : 0u;
+                const uint32_t ent = ce[k] = act[k] ? cl[c] : 0u;
                 v[k] = (uint32_t)(tw * 32) + (ent & 1023u);
                 // record slot: rank of v among the degree > 0 vertices
                 const uint32_t slot = __shfl_sync(full, prel, (ent >> 5) & 31) + (ent >> 10);
@@ -1116,16 +1062,14 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
                     cnt.add(found, (int64_t)j, (int64_t)h[k].x, max_pos);
                 }
                 const unsigned m = __ballot_sync(full, open);
-                if (m) {
-                    if (open) ol[nopen + __popc(m & lt)] = make_uint2(v[k], h[k].x);
-                    nopen += __popc(m);
-                    __syncwarp();
-                    if (nopen >= 32u)
-                        bu_drain<OffT, LV, PF>(A, bm, ol, nopen, tw, s_found, max_pos, depth1, cnt);
-                }
+                if (open) ol[nopen + __popc(m & lt)] = (uint16_t)ce[k];
+                nopen += __popc(m);
             }
+            __syncwarp();
+            const bool last = b + 32 * C >= T;
+            while (nopen >= 32u || (last && nopen))
+                bu_drain<OffT, PF>(A, bm, ol, nopen, tw, prel, s_found, max_pos, depth1, lv, cnt);
         }
-        while (nopen) bu_drain<OffT, LV, PF>(A, bm, ol, nopen, tw, s_found, max_pos, depth1, cnt);
         __syncwarp();
         const uint32_t f = s_found[lane];
         if (valid && f) {
@@ -1586,10 +1530,10 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                 }
             }
             BuSmem &bs = *reinterpret_cast<BuSmem *>(dsm);  // the top-down staging area is idle
-            if (SCAN && S.v_f * 64 < A.n)  // small frontier: open rows are mostly scanned to their end
-                phase_bu<OffT, K, kLaneVecsScan, PART>(A, S, in, out, spare, ctr, red, sf, bs);
-            else
-                phase_bu<OffT, K, kLaneVecs, PART>(A, S, in, out, spare, ctr, red, sf, bs);
+            // rows walked per lane before the cooperative scan: 2 vectors, 4 behind
+            // a small frontier (there most open rows are scanned to their end)
+            phase_bu<OffT, K, PART>(A, S, in, out, spare, ctr, red, sf, bs,
+                                    SCAN && S.v_f * 64 < A.n ? kLaneVecsScan : kLaneVecs);
         }
         grid.sync();
 
@@ -1651,14 +1595,14 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
 
 // One rank's bottom-up layer with the persistent kernel's tile machinery
 // (phase_bu<PART>): called by hbfs_part_bu (csrc/part.cu) as a plain launch.
-template <typename OffT, int K, int LV>
+template <typename OffT, int K>
 __global__ void __launch_bounds__(kBlock, 2) part_bu_kernel(Args<OffT> A, St S, Ctr *ctr, const uint32_t *inp,
-                                                          uint32_t *outp) {
+                                                          uint32_t *outp, int lv) {
     __shared__ unsigned long long red[(kBlock / 32) * 4];
     __shared__ uint32_t s_found[kBlock];
     __shared__ BuSmem bs;
-    phase_bu<OffT, K, LV, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
-                                ctr, red, s_found + (threadIdx.x & ~31), bs);
+    phase_bu<OffT, K, true>(A, S, Plane{const_cast<uint32_t *>(inp)}, Plane{outp}, Plane{nullptr},
+                            ctr, red, s_found + (threadIdx.x & ~31), bs, lv);
 }
 
 // Ctr (found << 35 | degree sum, gathers, fallbacks) -> {found, degree sum, gathers, fallbacks}
@@ -1707,15 +1651,14 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, part_bu_kernel<uint64_t, 2, kLaneVecs>,
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, part_bu_kernel<uint64_t, 2>,
                                                               kBlock, 0));
         grid = std::max(1, per_sm) * sms;
     }
     uint32_t *outp = next_slice - wlo;
-    if (v_f >= 0 && v_f * 64 < n)  // tiny frontier: rows are mostly scanned to their end
-        part_bu_kernel<uint64_t, 2, kLaneVecsScan><<<grid, kBlock, 0, st>>>(A, S, ctr, F, outp);
-    else
-        part_bu_kernel<uint64_t, 2, kLaneVecs><<<grid, kBlock, 0, st>>>(A, S, ctr, F, outp);
+    // tiny frontier: rows are mostly scanned to their end
+    part_bu_kernel<uint64_t, 2><<<grid, kBlock, 0, st>>>(A, S, ctr, F, outp,
+                                                        v_f >= 0 && v_f * 64 < n ? kLaneVecsScan : kLaneVecs);
     part_bu_counters<<<1, 1, 0, st>>>(ctr, counters);
     HB_CUDA(cudaGetLastError());
     return HBFS_OK;
