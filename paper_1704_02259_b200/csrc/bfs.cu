@@ -110,6 +110,7 @@ struct Args {
     const uint4 *hd;      // head records (common.cuh), rank order over the degree > 0 vertices
     const uint32_t *pre;  // records before bitmap word w (indexed like posw)
     int64_t n, nw, arcs, ncs;
+    int64_t n_pos;        // vertices with degree > 0 (head records)
     uint32_t *parent;
     int32_t *level;
     uint32_t *bits;  // planes vis | B0 | B1 | B2, nw words each
@@ -124,6 +125,7 @@ struct Args {
     Heur H;
     int max_pos, use_simd, parent_mode, do_init;
     int direct_levels;  // 1: stamp levels at discovery (small graphs), 0: final pass
+    int64_t bu_exec_ratio;       // top-down layers run bottom-up when candidates <= ratio * e_f (0: never)
     int64_t part_w0, part_wend;  // partition (PART): owned word range
     int64_t part_lo, part_nown;  // partition (PART): owned vertex range
     uint32_t *cand, *touch;      // partition top-down: remote targets' min parent / touched bits
@@ -895,6 +897,10 @@ struct TileSched {
     }
 };
 
+// Top-down layers over a bitmap frontier run bottom-up when the candidates
+// left are at most this many times the frontier's arcs.
+constexpr int64_t kBuExecRatio = 2;
+
 constexpr int kOpenCap = 160;  // open-list entries per warp: < 32 pending + one round's pushes (<= 32 * 4)
 
 // Bottom-up shared memory (aliases the top-down staging area, idle then).
@@ -1472,7 +1478,18 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         // SQ: the frontier queue's size (the layer's counts on one GPU; the
         // rank's own share, from the conversion, in a partition)
         St SQ = S;
-        if (dir == HBFS_TOP_DOWN && (PART || S.kind == 1)) {
+        // How the layer is executed (the trace reports `dir`): a top-down layer
+        // whose frontier is only a bitmap (it follows a bottom-up or harvest
+        // layer) would first convert it to a queue, an O(n) sweep like a
+        // bottom-up layer's; when few candidates are left — unvisited vertices
+        // with degree > 0 — the bottom-up sweep alone is cheaper and finds the
+        // same vertices with the same parents (first hit in a sorted row =
+        // smallest frontier neighbour).  SCALE 26: such layers 100-200 -> 30 us.
+        int xdir = dir;
+        if (!PART && xdir == HBFS_TOP_DOWN && S.kind == 1 && A.bu_exec_ratio > 0 &&
+            S.eu_v - (A.n - A.n_pos) <= A.bu_exec_ratio * S.e_f)
+            xdir = HBFS_BOTTOM_UP;
+        if (xdir == HBFS_TOP_DOWN && (PART || S.kind == 1)) {
             phase_convert<OffT, PART>(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
             grid.sync();
             STAMP(1);
@@ -1482,7 +1499,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
                 SQ.e_f = (int64_t)(cv & kPackMask);
             }
         }
-        const bool cb = dir == HBFS_TOP_DOWN && A.cb_ranges > 1 && SQ.e_f >= A.cb_min_arcs &&
+        const bool cb = xdir == HBFS_TOP_DOWN && A.cb_ranges > 1 && SQ.e_f >= A.cb_min_arcs &&
                         SQ.v_f <= kCbMaxF;
         // Slot (L+1)%3 was last read right after the barrier that ended layer
         // L-2, so every CTA is past that read; it must be zero when layer L+1
@@ -1493,14 +1510,14 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             if (!PART) A.ctl->conv = 0;  // PART: the host resets it (other CTAs read it above)
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
-        const bool harvest = dir == HBFS_TOP_DOWN && SQ.e_f >= A.harvest_min_arcs;
+        const bool harvest = xdir == HBFS_TOP_DOWN && SQ.e_f >= A.harvest_min_arcs;
         if (cb) {
             phase_cb_build<OffT, PART>(A, SQ, spare, (int)(L & 1));
             grid.sync();
             STAMP(2);
             if (harvest) phase_cb_run<OffT, true, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
             else phase_cb_run<OffT, false, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
-        } else if (dir == HBFS_TOP_DOWN) {
+        } else if (xdir == HBFS_TOP_DOWN) {
             if (harvest) {
                 td_prologue<OffT, PART>(A, SQ, spare);
                 grid.sync();  // vis now holds the frontier: the expansion tests vis alone
@@ -1515,7 +1532,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             STAMP(3);
             phase_harvest<OffT, PART>(A, out, &ctr->packed, red, (int32_t)L + 1);
         }
-        if (dir == HBFS_BOTTOM_UP) {
+        if (xdir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
             const Plane vis_all{A.bits};
             if (PART) {  // the owned-word tiles do not cover the replicated planes:
@@ -1571,7 +1588,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         S.eu_v -= nvf;
         S.eu_e -= nef;
         S.dir = dir;
-        S.kind = (dir == HBFS_TOP_DOWN && !harvest) ? 0 : 1;  // harvest builds no queue
+        S.kind = (xdir == HBFS_TOP_DOWN && !harvest) ? 0 : 1;  // harvest and bottom-up build no queue
         S.layer = L + 1;
         ++rows;
     }
@@ -1811,6 +1828,8 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.posw = g->posw.as<uint32_t>();
     A.hd = g->hd.as<uint4>();
     A.pre = g->pre.as<uint32_t>();
+    A.n_pos = g->n_pos;
+    A.bu_exec_ratio = env_i64("HBFS_BU_EXEC_RATIO", kBuExecRatio);
     A.n = g->n;
     A.nw = g->nw;
     A.arcs = g->arcs;

@@ -148,7 +148,7 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
 // graph (graph_finalize / part build); synchronises the stream.
 constexpr int kHeadLen = 3;
 int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
-                DevBuf &pre, DevBuf &hd, cudaStream_t st);
+                DevBuf &pre, DevBuf &hd, cudaStream_t st, int64_t *n_records = nullptr);
 
 // Bottom-up layer of one partition rank with the persistent kernel's tile
 // machinery (defined in bfs.cu, used by part.cu).  v_f: global frontier size
@@ -180,6 +180,7 @@ struct hbfs_graph {
     int64_t arcs = 0;
     int64_t m_edges = 0;   // TEPS denominator (csr.py:73)
     int64_t max_degree = 0;
+    int64_t n_pos = 0;     // vertices with degree > 0 (= head records)
     int wide = 0;          // 1: 64-bit offsets (arcs >= 2^32), else 32-bit
     int device = 0;
     hbfs::DevBuf rs;       // OffT[n+1]

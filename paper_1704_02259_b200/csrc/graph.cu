@@ -224,7 +224,7 @@ __global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, const ui
 }
 
 int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
-                DevBuf &pre, DevBuf &hd, cudaStream_t st) {
+                DevBuf &pre, DevBuf &hd, cudaStream_t st, int64_t *n_records) {
     static_assert(kHeadLen == 3, "head record layout");
     const int64_t nw = (n + 31) / 32;
     HB_CHECK(pre.alloc((nw + 1) * 4 + 16));
@@ -241,6 +241,7 @@ int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const 
         HB_CUDA(cudaMemcpyAsync(&total, pre.as<uint32_t>() + nw, 4, cudaMemcpyDeviceToHost, st));
         HB_CUDA(cudaStreamSynchronize(st));
     }
+    if (n_records) *n_records = (int64_t)total;
     HB_CHECK(hd.alloc(((size_t)total + 1) * sizeof(uint4)));
     if (n <= 0) return HBFS_OK;
     const int blocks = grid_for(n);
@@ -311,7 +312,7 @@ int graph_finalize(hbfs_graph *g, cudaStream_t st) {
     if (g->max_degree >= (int64_t(1) << 32))
         return set_error(HBFS_ECAPACITY, "a row of %lld entries exceeds the 32-bit degree of the head records",
                          (long long)g->max_degree);
-    HB_CHECK(build_heads(g->n, g->rs.p, g->wide, g->adj.as<uint32_t>(), g->posw.as<uint32_t>(), g->pre, g->hd, st));
+    HB_CHECK(build_heads(g->n, g->rs.p, g->wide, g->adj.as<uint32_t>(), g->posw.as<uint32_t>(), g->pre, g->hd, st, &g->n_pos));
     return HBFS_OK;
 }
 

@@ -84,6 +84,10 @@ KNOBS = {
     "defer": {"HBFS_DEFER_LEVELS_MIN_N": "0"},
     # the large-graph kernel variant (2 searches/lane, scan-tuned bottom-up)
     "scan_variant": {"HBFS_KERNEL_VARIANT": "3"},
+    # every top-down layer over a bitmap frontier executed by the bottom-up sweep
+    # (normally only when few candidates are left); the trace still says top-down
+    "bu_exec": {"HBFS_BU_EXEC_RATIO": str(1 << 40)},
+    "no_bu_exec": {"HBFS_BU_EXEC_RATIO": "0"},
 }
 
 
