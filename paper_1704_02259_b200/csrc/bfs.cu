@@ -678,7 +678,9 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
                         remote_arc(A, v[k], u[k]);
                         continue;
                     }
-                    atomicOr(&out[v[k] >> 5], b);
+                    // one GPU: the harvest finds the reached vertices by their
+                    // parents (no longer NIL), so an arc costs one reduction, not two
+                    if (PART) atomicOr(&out[v[k] >> 5], b);
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
                 }
@@ -1226,10 +1228,17 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
     }
 }
 
-// Harvest after a fire-and-forget top-down expansion: the next-frontier bits
-// were set by reductions (a vertex was discovered iff it was unvisited before
-// the layer and some frontier arc reached it).  Thread per word: vis commit,
-// count and degree sum of the found vertices (and their levels on small graphs).
+// Harvest after a fire-and-forget top-down expansion: a vertex was discovered
+// iff it was unvisited before the layer and some frontier arc reached it, i.e.
+// iff its parent is no longer NIL.  A warp takes a tile of 32 bitmap words;
+// round r reads the parents of word r's unvisited degree > 0 vertices (lane =
+// bit: one coalesced 128-byte load) and the ballot of "parent set" is that
+// word's share of the next frontier.  Then per word: next-frontier and vis
+// words, count and degree sum of the found vertices (and their levels on small
+// graphs).  Reading the parents (268 MB at SCALE 26, streamed) instead of a
+// next-frontier bitmap set by a second reduction per arc: the expansion is
+// bound by the SM's L2 request rate (1 load + 1.5 per reduction, tools/mb).
+// Partitions (PART) keep the bitmap reductions: thread per word.
 template <typename OffT, bool PART = false>
 __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
                               unsigned long long *red, int32_t depth1) {
@@ -1238,27 +1247,79 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
     const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw;
-    // four words per thread per step: their loads (and the vis words') in flight together
-    for (int64_t w0 = wa + tid; w0 < wb; w0 += 4 * nth) {
-        uint32_t bits[4], vw[4];
+    if (!PART) {
+        const unsigned full = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        const int64_t ntiles = (wb - wa + 31) >> 5;
+        for (int64_t tile = tid >> 5; tile < ntiles; tile += nth >> 5) {
+            const int64_t tw = wa + tile * 32, wl = tw + lane;
+            const bool valid = wl < wb;
+            const uint32_t vw = valid ? vis[wl] : ~0u;
+            const uint32_t candl = valid ? ~vw & __ldg(A.posw + wl) : 0u;
+            uint32_t f = 0;
+            if (!__any_sync(full, candl != 0)) continue;
+#pragma unroll 1
+            for (int r0 = 0; r0 < 32; r0 += 8) {  // 8 words' parent loads in flight together
+                // per candidate (lane = bit, so each is one coalesced load per
+                // word): its parent and, without waiting for it, its row bounds
+                // — the degree counts only if the vertex turns out reached
+                uint32_t p[8];
+                OffT d[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t w = w0 + j * nth;
-            bits[j] = w < wb ? __ldcg(&out[w]) : 0u;  // set by the expansion's reductions
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) vw[j] = bits[j] ? vis[w0 + j * nth] : 0u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!bits[j]) continue;
-            const int64_t w = w0 + j * nth;
-            vis[w] = vw[j] | bits[j];
-            acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
-            if (A.direct_levels)
-                for (uint32_t x = bits[j]; x; x &= x - 1) {
-                    HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
-                    A.level[w * 32 + __ffs(x) - 1] = depth1;
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t cm = __shfl_sync(full, candl, r0 + j);
+                    p[j] = HBFS_NIL;
+                    d[j] = 0;
+                    if ((cm >> lane) & 1u) {
+                        const int64_t v = (tw + r0 + j) * 32 + lane;
+                        p[j] = __ldcg(A.parent + v);
+                        d[j] = __ldg(A.rs + v + 1) - __ldg(A.rs + v);
+                    }
                 }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (p[j] == HBFS_NIL) d[j] = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t fm = __ballot_sync(full, p[j] != HBFS_NIL);
+                    if (lane == r0 + j) f = fm;
+                    acc += (unsigned long long)d[j];
+                }
+            }
+            if (f) {
+                out[wl] = f;
+                vis[wl] = vw | f;
+                acc += (unsigned long long)__popc(f) << kPackShift;
+                if (A.direct_levels)
+                    for (uint32_t x = f; x; x &= x - 1) {
+                        HB_DCHECK(wl * 32 + __ffs(x) - 1 < A.n, 0);
+                        A.level[wl * 32 + __ffs(x) - 1] = depth1;
+                    }
+            }
+        }
+    } else {
+        // four words per thread per step: their loads (and the vis words') in flight together
+        for (int64_t w0 = wa + tid; w0 < wb; w0 += 4 * nth) {
+            uint32_t bits[4], vw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t w = w0 + j * nth;
+                bits[j] = w < wb ? __ldcg(&out[w]) : 0u;  // set by the expansion's reductions
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) vw[j] = bits[j] ? vis[w0 + j * nth] : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!bits[j]) continue;
+                const int64_t w = w0 + j * nth;
+                vis[w] = vw[j] | bits[j];
+                acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
+                if (A.direct_levels)
+                    for (uint32_t x = bits[j]; x; x &= x - 1) {
+                        HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
+                        A.level[w * 32 + __ffs(x) - 1] = depth1;
+                    }
+            }
         }
     }
     acc = warp_sum(acc);
