@@ -208,6 +208,18 @@ def profiled_traffic(label):
         return None
 
 
+def modelled_bytes(label):
+    """Mean algorithmic bytes per traversal (SURVEY 8(d) B_sector over the 64
+    bench roots) of a workload, recorded by a single-GPU run of this script
+    (profiles/bytes_model.json): a property of graph, roots and direction
+    rule, so the partitioned run reports its roofline against the same bytes."""
+    try:
+        with open(os.path.join(REPO, "profiles", "bytes_model.json")) as fh:
+            return json.load(fh).get(label)
+    except (OSError, ValueError):
+        return None
+
+
 # --------------------------------------------------------------- reference
 
 def reference_roots_per_step(cfg, workers):
@@ -519,26 +531,26 @@ def run_distributed(args, cfg):
     ops = CudaRankOps.generate(params, ws, rank, device=dev)
     comm = TorchComm()
     db = NcclBfs(ops, ws, rank)  # the per-layer loop in C++ over NCCL (csrc/part.cu hbfs_mg_bfs)
-    # roots: identical on every rank (computed from the generator's graph on rank 0)
-    roots_t = torch.zeros(ROOTS, dtype=torch.int64, device=dev)
-    if rank == 0:
-        g = hb.generate_graph(params)
-        roots_t.copy_(torch.from_numpy(hb.sample_sources(g, ROOTS, 1).astype(np.int64)))
-        g.free()
-    dist.broadcast(roots_t, 0)
-    roots = [int(x) for x in roots_t.tolist()]
+    # roots: the reference's sampling order filtered by the degrees the ranks
+    # hold (identical on every rank; no rank builds the whole CSR)
+    from paper_1704_02259_b200.mgpu import sample_sources_partitioned
+
+    roots = [int(x) for x in sample_sources_partitioned([ops], comm, ROOTS, 1)]
     p = hb.HeuristicParams(**cfg["heur"])
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+    nlayers = []  # cooperative launches of one sweep = layers of its traversals
+
     def sweep():
         times = []
+        nlayers.clear()
         for s in roots:
             flush.fill_(1)
             dist.barrier()
             torch.cuda.synchronize()
             ev0.record()
-            db.bfs(s, p)
+            nlayers.append(len(db.bfs(s, p).trace))
             ev1.record()
             ev1.synchronize()
             times.append(comm.all_reduce_max_float(ev0.elapsed_time(ev1) * 1e-3))
@@ -558,7 +570,16 @@ def run_distributed(args, cfg):
     m = params.num_edges
     total = sum(per)
     value = len(per) * m / total / 1e9
-    # e2e: traversal + each rank's owned parent/level slice to host
+    # exchange volume per traversal (this rank): 8-byte records, the in-place
+    # all-gather of the next-frontier plane and the 32-byte counter all-reduce per layer
+    nv_bytes = 0
+    for s in roots:
+        db.bfs(s, p)
+        st = ops.exchange_stats()
+        wper = (((params.num_vertices + 31) // 32) + ws - 1) // ws
+        nv_bytes += 8 * st["records_sent"] + st["layers"] * (4 * wper * (ws - 1) + 32) + 16 * ws * st["record_exchanges"]
+    nv_bytes = comm.all_reduce_max_float(float(nv_bytes)) / len(roots)
+    # e2e: traversal + each rank's owned parent/level slice to host (pinned)
     e2e = []
     for s in roots:
         dist.barrier()
@@ -567,6 +588,20 @@ def run_distributed(args, cfg):
         db.outputs()
         e2e.append(comm.all_reduce_max_float(time.perf_counter() - t1))
     if rank == 0:
+        peak, peak_src = measured_peak()
+        bm = modelled_bytes(cfg["label"])
+        t_trav = total / len(per)
+        roof = None
+        if bm:
+            achieved = bm / t_trav / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
+                    "frac": achieved / (peak * ws), "traffic": None,
+                    "kernel": "bfs_kernel<PART> (one cooperative launch per layer and rank) + exchange",
+                    "bytes_per_launch": bm, "launch_ms": t_trav * 1e3,
+                    "peak_source": peak_src + f" x {ws} GPUs",
+                    "bytes_source": "profiles/bytes_model.json (B_sector of the same graph, roots and rule, single-GPU run)",
+                    "nvlink_bytes_per_traversal_per_rank": nv_bytes,
+                    "nvlink_gbs_per_rank": nv_bytes / t_trav / 1e9}
         line = {
             "metric": "harmonic-mean GTEPS over 64 roots", "value": value, "unit": "GTEPS",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -577,11 +612,12 @@ def run_distributed(args, cfg):
                        "roots": ROOTS, "heuristic": cfg["heur"], "parent_mode": "minid",
                        "parallelism": f"1d-partition x{ws} (C++ loop; NCCL all-gather / send-recv records / all-reduce)",
                        "l2": "flushed (256 MB write) before every traversal"},
-            "gpu_launches": None,
+            "gpu_launches": args.steps * sum(nlayers),
             "wall_s_timed_region": wall,
-            "roofline": None,
+            "roofline": roof,
             "e2e": {"value": len(e2e) * m / sum(e2e) / 1e9, "unit": "GTEPS",
-                    "h2d_bytes_per_step": 8 * ROOTS, "d2h_bytes_per_step": ROOTS * 8 * params.num_vertices},
+                    "h2d_bytes_per_step": 8 * ROOTS, "d2h_bytes_per_step": ROOTS * 8 * params.num_vertices,
+                    "call": "NcclBfs.bfs(root) + outputs(): each rank's owned parent/level slice into pinned host arrays"},
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

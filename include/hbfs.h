@@ -108,6 +108,10 @@ int hbfs_graph_free(hbfs_graph *g);
  * out (host pointer).  Returns HBFS_EINVAL if too few eligible vertices. */
 int hbfs_sample_sources(const hbfs_graph *g, int64_t count, uint64_t seed, int allow_isolated,
                         uint32_t *out);
+/* The first `count` ids of that sampling order alone (no graph, no O(n) memory):
+ * partitioned graphs filter them by the degrees their ranks hold
+ * (hbfs_part_degrees; mgpu.sample_sources_partitioned). */
+int hbfs_source_order_prefix(int64_t n, uint64_t seed, int64_t count, uint32_t *out);
 
 /* ---- traversal (L2-L4): replaces hybrid.hybrid_bfs (hybrid.py:83-175) and its
  * per-layer engine.run_* dispatch (engine.py:81-155).  The whole traversal runs
@@ -214,6 +218,8 @@ int hbfs_part_info(const hbfs_part *p, int64_t *n, int64_t *lo, int64_t *hi,
                    int64_t *local_arcs, int64_t *m_edges);
 /* Degree of v if owned, else 0. */
 int hbfs_part_degree(const hbfs_part *p, int64_t v, int64_t *deg);
+/* deg[i] = degree of ids[i] if owned, else 0 (host arrays of `count` entries). */
+int hbfs_part_degrees(const hbfs_part *p, const uint32_t *ids, int64_t count, int64_t *deg);
 int hbfs_part_free(hbfs_part *p);
 /* Per-root reset: parent/level/frontier/visited with the root. */
 int hbfs_part_init(hbfs_part *p, int64_t root, void *stream);
@@ -263,6 +269,11 @@ int hbfs_mg_bfs(hbfs_mg *m, hbfs_part *p, int64_t root, const hbfs_params *param
 int hbfs_mgl_bfs(hbfs_part **parts, int32_t world, int64_t root, const hbfs_params *params,
                  hbfs_layer_row *trace, int64_t trace_cap, int64_t *n_layers, float *device_ms,
                  void *stream);
+/* Exchange volume of the last traversal of this part through either loop:
+ * out[0] records sent (8 bytes each), out[1] records received, out[2] layers
+ * (one next-frontier all-gather + one counter all-reduce each), out[3]
+ * top-down record exchanges. */
+int hbfs_part_exchange_stats(const hbfs_part *p, int64_t *out);
 
 #ifdef __cplusplus
 }

@@ -64,6 +64,7 @@ SIGNATURES = {
     "hbfs_graph_export": (C.c_int, [P, P, P, C.c_int, P]),
     "hbfs_graph_free": (C.c_int, [P]),
     "hbfs_sample_sources": (C.c_int, [P, i64, u64, C.c_int, P]),
+    "hbfs_source_order_prefix": (C.c_int, [i64, u64, i64, P]),
     "hbfs_bfs": (C.c_int, [P, i64, C.POINTER(hbfs_params), P, P, C.c_int, P, i64, P, P, P]),
     "hbfs_validate": (C.c_int, [P, i64, P, P, C.c_int, C.c_int, P, P, P]),
     "hbfs_traversal_bytes": (C.c_int, [P, i64, P, P, i64, P, P, P]),
@@ -81,6 +82,7 @@ SIGNATURES = {
     "hbfs_part_from_csr": (C.c_int, [P, P, i64, i64, i64, i64, P, C.POINTER(P)]),
     "hbfs_part_info": (C.c_int, [P, P, P, P, P, P]),
     "hbfs_part_degree": (C.c_int, [P, i64, P]),
+    "hbfs_part_degrees": (C.c_int, [P, P, i64, P]),
     "hbfs_part_free": (C.c_int, [P]),
     "hbfs_part_init": (C.c_int, [P, i64, P]),
     "hbfs_part_bu": (C.c_int, [P, i32, i32, P, P, P]),
@@ -95,6 +97,7 @@ SIGNATURES = {
     "hbfs_mg_free": (C.c_int, [P]),
     "hbfs_mg_bfs": (C.c_int, [P, P, i64, C.POINTER(hbfs_params), P, i64, P, P, P]),
     "hbfs_mgl_bfs": (C.c_int, [P, i32, i64, C.POINTER(hbfs_params), P, i64, P, P, P]),
+    "hbfs_part_exchange_stats": (C.c_int, [P, P]),
 }
 
 _lib = None

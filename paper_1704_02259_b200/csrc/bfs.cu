@@ -1547,9 +1547,10 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         // same vertices with the same parents (first hit in a sorted row =
         // smallest frontier neighbour).  SCALE 26: such layers 100-200 -> 30 us.
         int xdir = dir;
-        if (!PART && xdir == HBFS_TOP_DOWN && S.kind == 1 && A.bu_exec_ratio > 0 &&
-            S.eu_v - (A.n - A.n_pos) <= A.bu_exec_ratio * S.e_f)
-            xdir = HBFS_BOTTOM_UP;
+        // (partitions: the frontier is always a bitmap, the sweep stays local to
+        // the rank, and the host loop takes the same decision — bu_executes — to
+        // skip the record exchange)
+        if (bu_executes(xdir, S.kind, S.eu_v, S.e_f, A.n, A.n_pos, A.bu_exec_ratio)) xdir = HBFS_BOTTOM_UP;
         if (xdir == HBFS_TOP_DOWN && (PART || S.kind == 1)) {
             phase_convert<OffT, PART>(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
             grid.sync();
@@ -1803,6 +1804,8 @@ static int64_t env_i64(const char *name, int64_t dflt) {
     return e ? atoll(e) : dflt;
 }
 
+int64_t bu_exec_ratio() { return env_i64("HBFS_BU_EXEC_RATIO", kBuExecRatio); }
+
 template <typename OffT>
 static size_t dyn_smem_bytes() {
     size_t b = sizeof(TdSmem<OffT>);  // top-down phases; bottom-up: open lists + candidate lists
@@ -1890,7 +1893,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.hd = g->hd.as<uint4>();
     A.pre = g->pre.as<uint32_t>();
     A.n_pos = g->n_pos;
-    A.bu_exec_ratio = env_i64("HBFS_BU_EXEC_RATIO", kBuExecRatio);
+    A.bu_exec_ratio = bu_exec_ratio();
     A.n = g->n;
     A.nw = g->nw;
     A.arcs = g->arcs;
@@ -2008,9 +2011,9 @@ struct PartTrav {
     size_t smem = 0;
     DevBuf bits, q, qo, qr, cs, cbq, cbqo, cbqr, cbcs, ctl, phases;
     Args<uint64_t> A;
-    Ctr *h_ctr = nullptr;  // pinned: the last layer's counters (valid after a stream sync)
+    void *h_state = nullptr;  // pinned staging of the controller state written before each launch
     ~PartTrav() {
-        if (h_ctr) cudaFreeHost(h_ctr);
+        if (h_state) cudaFreeHost(h_state);
     }
 };
 
@@ -2044,7 +2047,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     }
     if (!rc) rc = T->ctl.alloc(ctl_bytes());
     if (!rc) rc = T->phases.alloc((kRowsCap + 1) * kPhaseSlots * 8);
-    if (!rc && cudaMallocHost(&T->h_ctr, sizeof(Ctr)) != cudaSuccess) rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
+    if (!rc && cudaMallocHost(&T->h_state, 256) != cudaSuccess) rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
     if (!rc) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
@@ -2115,19 +2118,26 @@ uint32_t *part_trav_plane(void *h, int64_t depth) {
 }
 
 // One layer, asynchronous: the global controller state in; this rank's
-// counters ({found, their degree sum, gathers, fallbacks}) from
-// part_trav_counters once the stream has been synchronised; direction =
-// decide(state).
-void part_trav_counters(void *h, unsigned long long counters[4]) {
-    const Ctr &c = *static_cast<PartTrav *>(h)->h_ctr;
-    counters[0] = c.packed >> kPackShift;
-    counters[1] = c.packed & kPackMask;
-    counters[2] = c.gathers;
-    counters[3] = c.fallbacks;
+// counters stay on the device — part_trav_add_counters folds them into the
+// layer's totals ({found, their degree sum, gathers, fallbacks}) on the
+// stream; direction = decide(state).
+__global__ void k_add_layer_counters(const Ctr *c, const unsigned long long *applied, unsigned long long *tot) {
+    atomicAdd(&tot[0], (c->packed >> kPackShift) + (applied ? applied[0] : 0ull));
+    atomicAdd(&tot[1], (c->packed & kPackMask) + (applied ? applied[1] : 0ull));
+    atomicAdd(&tot[2], c->gathers);
+    atomicAdd(&tot[3], c->fallbacks);
+}
+
+int part_trav_add_counters(void *h, int64_t layer, const unsigned long long *applied, unsigned long long *tot,
+                           cudaStream_t st) {
+    PartTrav *T = static_cast<PartTrav *>(h);
+    k_add_layer_counters<<<1, 1, 0, st>>>(&T->A.ctl->ctr[layer % 3], applied, tot);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
 }
 
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, cudaStream_t st) {
+                    const hbfs_params *p, int64_t n_pos_global, cudaStream_t st) {
     PartTrav *T = static_cast<PartTrav *>(h);
     Args<uint64_t> A = T->A;
     A.H.heuristic = p->heuristic;
@@ -2141,6 +2151,8 @@ int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, u
     A.parent_mode = HBFS_PARENT_MINID;
     A.root = root;
     A.do_init = do_init;
+    A.n_pos = n_pos_global;
+    A.bu_exec_ratio = bu_exec_ratio();
     struct {
         int64_t layer, v_f, e_f, eu_v, eu_e, prev_vf;
         int32_t dir, kind, done;
@@ -2149,10 +2161,13 @@ int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, u
         unsigned long long conv;
     } hs = {state[0], state[1], state[2], state[3], state[4], state[5], dir, 1, 0, 0u, 0, 0ull};
     static_assert(offsetof(Ctl, conv) + sizeof(unsigned long long) == sizeof(hs), "Ctl head layout");
-    HB_CUDA(cudaMemcpyAsync(A.ctl, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+    static_assert(sizeof(hs) <= 256, "state staging");
+    // pinned staging: the caller synchronises the stream once per layer, so the
+    // previous layer's copy has been consumed
+    memcpy(T->h_state, &hs, sizeof(hs));
+    HB_CUDA(cudaMemcpyAsync(A.ctl, T->h_state, sizeof(hs), cudaMemcpyHostToDevice, st));
     void *kargs[] = {&A};
     HB_CUDA(cudaLaunchCooperativeKernel(part_kernel(), dim3(T->grid), dim3(kBlock), kargs, T->smem, st));
-    HB_CUDA(cudaMemcpyAsync(T->h_ctr, &A.ctl->ctr[state[0] % 3], sizeof(Ctr), cudaMemcpyDeviceToHost, st));
     return HBFS_OK;
 }
 

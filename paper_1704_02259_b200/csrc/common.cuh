@@ -150,6 +150,19 @@ constexpr int kHeadLen = 3;
 int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
                 DevBuf &pre, DevBuf &hd, cudaStream_t st, int64_t *n_records = nullptr);
 
+// A top-down layer whose frontier is only a bitmap (kind 1) runs as a
+// bottom-up sweep when at most ratio * e_f candidates are left (unvisited
+// vertices with degree > 0): same vertices, same parents (bfs.cu).  Host +
+// device: the multi-GPU loop mirrors the kernel's choice.
+__host__ __device__ inline bool bu_executes(int dir, int kind, int64_t eu_v, int64_t e_f, int64_t n,
+                                            int64_t n_pos, int64_t ratio) {
+    const int64_t cand = eu_v - (n - n_pos);
+    // few candidates in absolute terms too: a sweep over many candidates behind a
+    // small hub frontier scans their rows to the end
+    return dir == HBFS_TOP_DOWN && kind == 1 && ratio > 0 && cand <= ratio * e_f && cand * 64 <= n;
+}
+int64_t bu_exec_ratio();  // HBFS_BU_EXEC_RATIO or the default
+
 // Bottom-up layer of one partition rank with the persistent kernel's tile
 // machinery (defined in bfs.cu, used by part.cu).  v_f: global frontier size
 // (< 0: unknown).  scratch: part_bu_scratch_bytes() of device memory.
@@ -169,8 +182,10 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
 void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, cudaStream_t st);  // asynchronous
-void part_trav_counters(void *h, unsigned long long counters[4]);  // after a stream sync
+                    const hbfs_params *p, int64_t n_pos_global, cudaStream_t st);  // asynchronous
+// tot[0..3] += this rank's counters of `layer` (+ applied[0..1], the records it applied), on the stream
+int part_trav_add_counters(void *h, int64_t layer, const unsigned long long *applied, unsigned long long *tot,
+                           cudaStream_t st);
 
 }  // namespace hbfs
 

@@ -799,6 +799,63 @@ extern "C" int hbfs_graph_free(hbfs_graph *g) {
     HB_ENTRY_END
 }
 
+// ids whose source-order key lies below `limit`, appended in any order
+__global__ void k_order_below(int64_t n, uint64_t seed, uint64_t limit, unsigned long long *cnt, int64_t cap,
+                              uint32_t *ids, uint64_t *keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = hbfs::mix64(hbfs::mix64((uint64_t)i + 0x5EEDu) ^ seed);
+        if (k < limit) {
+            const unsigned long long at = atomicAdd(cnt, 1ull);
+            if ((int64_t)at < cap) {
+                ids[at] = (uint32_t)i;
+                keys[at] = k;
+            }
+        }
+    }
+}
+
+// The first `count` ids of the source sampling order argsort(mix64(mix64(id +
+// 0x5EED) ^ seed)) (harness.py:85-87) without sorting all n keys or touching
+// a graph: the keys are uniform, so a threshold keeps about 4 * count of them.
+// For partitioned graphs (mgpu.sample_sources_partitioned), where no rank
+// holds every degree.
+extern "C" int hbfs_source_order_prefix(int64_t n, uint64_t seed, int64_t count, uint32_t *out) {
+    HB_ENTRY_BEGIN
+    clear_error();
+    if (!out || count < 0 || count > n) return set_error(HBFS_EINVAL, "bad arguments");
+    if (count == 0) return HBFS_OK;
+    const int64_t cap = 8 * count + 1024;
+    DevBuf cnt, ids, keys;
+    HB_CHECK(cnt.alloc(8));
+    HB_CHECK(ids.alloc(cap * 4));
+    HB_CHECK(keys.alloc(cap * 8));
+    std::vector<uint32_t> hi(cap);
+    std::vector<uint64_t> hk(cap);
+    for (double want = 4.0 * (double)count + 256;; want *= 2) {
+        const double frac = want / (double)n;
+        const uint64_t limit = frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551615.0);
+        HB_CUDA(cudaMemset(cnt.p, 0, 8));
+        k_order_below<<<grid_for(n), 256>>>(n, seed, limit, cnt.as<unsigned long long>(), cap, ids.as<uint32_t>(),
+                                          keys.as<uint64_t>());
+        HB_CUDA(cudaGetLastError());
+        unsigned long long got = 0;
+        HB_CUDA(cudaMemcpy(&got, cnt.p, 8, cudaMemcpyDeviceToHost));
+        if ((int64_t)got > cap) return set_error(HBFS_ECUDA, "source order: threshold kept too many keys");
+        if ((int64_t)got < count && limit != ~0ull) continue;  // too few: widen
+        HB_CUDA(cudaMemcpy(hi.data(), ids.p, got * 4, cudaMemcpyDeviceToHost));
+        HB_CUDA(cudaMemcpy(hk.data(), keys.p, got * 8, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> idx(got);
+        for (size_t i = 0; i < got; ++i) idx[i] = (int64_t)i;
+        std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+            return hk[a] != hk[b] ? hk[a] < hk[b] : hi[a] < hi[b];
+        });
+        for (int64_t i = 0; i < count; ++i) out[i] = hi[idx[i]];
+        return HBFS_OK;
+    }
+    HB_ENTRY_END
+}
+
 extern "C" int hbfs_sample_sources(const hbfs_graph *g, int64_t count, uint64_t seed,
                                    int allow_isolated, uint32_t *out) {
     HB_ENTRY_BEGIN

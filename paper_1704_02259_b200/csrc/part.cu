@@ -45,6 +45,7 @@ struct Part {
     DevBuf scratch;           // counters etc.
     DevBuf posw;              // uint32[wloc] deg > 0 bits of the owned vertices
     DevBuf hd, pre;           // head records of the owned rows, rank order + per-word prefix (common.cuh)
+    int64_t n_pos = 0;        // owned vertices with degree > 0
     DevBuf bu_scratch;        // part_bu_launch scratch (Ctl)
     int64_t fhint = -1;       // global frontier size of the next bottom-up layer (-1: unknown)
     // top-down exchange state (all kept clean between layers)
@@ -59,7 +60,9 @@ struct Part {
     void *trav = nullptr;     // persistent-kernel traversal state (bfs.cu part_trav_*)
     DevBuf recs_s, recs_r, acnt;  // records out / in, apply counters
     DevBuf counts_dev;        // int64[2 * world] record counts sent / received
-    unsigned long long *h_acnt = nullptr;  // pinned: apply counters of the last layer
+    unsigned long long *h_acnt = nullptr;  // pinned: the layer's counter totals (after the layer's stream sync)
+    DevBuf lay;                            // device: the layer's counter totals, uint64[4]
+    int64_t stat[4] = {0, 0, 0, 0};        // last traversal: records sent, received, layers, record exchanges
     size_t cap_s = 0, cap_r = 0;
     ~Part() {
         if (trav) part_trav_free(trav);
@@ -425,7 +428,7 @@ static int part_alloc_state(Part *P) {
     HB_CHECK(P->bu_scratch.alloc(part_bu_scratch_bytes()));
     HB_CUDA(cudaDeviceSynchronize());  // rs was built on the caller's stream
     kp_posw<<<pgrid(P->wloc), 256>>>(P->nloc, P->wloc, P->rs.as<uint64_t>(), P->posw.as<uint32_t>());
-    HB_CHECK(build_heads(P->nloc, P->rs.p, 1, P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->pre, P->hd, 0));
+    HB_CHECK(build_heads(P->nloc, P->rs.p, 1, P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->pre, P->hd, 0, &P->n_pos));
     {
         const int64_t nseg = P->arcs / kSegArcs + P->nloc / 1024 + 16;
         HB_CHECK(P->seg_u.alloc(nseg * 4));
@@ -630,6 +633,43 @@ extern "C" int hbfs_part_degree(const hbfs_part *P, int64_t v, int64_t *deg) {
     uint64_t h[2];
     HB_CUDA(cudaMemcpy(h, P->rs.as<uint64_t>() + (v - P->lo), 16, cudaMemcpyDeviceToHost));
     *deg = (int64_t)(h[1] - h[0]);
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+__global__ void kp_degrees(int64_t count, const uint32_t *ids, int64_t lo, int64_t hi, const uint64_t *rs,
+                           int64_t *deg) {
+    PSTRIDE(i, count) {
+        const int64_t v = ids[i];
+        deg[i] = v >= lo && v < hi ? (int64_t)(rs[v - lo + 1] - rs[v - lo]) : 0;
+    }
+}
+
+// deg[i] = degree of ids[i] if this rank owns it, else 0 (host arrays): summed
+// over the ranks these are the global degrees of a candidate list.
+extern "C" int hbfs_part_degrees(const hbfs_part *P, const uint32_t *ids, int64_t count, int64_t *deg) {
+    HB_ENTRY_BEGIN
+    if (!P || !ids || !deg || count < 0) return set_error(HBFS_EINVAL, "bad arguments");
+    if (count == 0) return HBFS_OK;
+    DevBuf di, dd;
+    HB_CHECK(di.alloc(count * 4));
+    HB_CHECK(dd.alloc(count * 8));
+    HB_CUDA(cudaMemcpy(di.p, ids, count * 4, cudaMemcpyHostToDevice));
+    kp_degrees<<<pgrid(count), 256>>>(count, di.as<uint32_t>(), P->lo, P->hi, P->rs.as<uint64_t>(), dd.as<int64_t>());
+    HB_CUDA(cudaGetLastError());
+    HB_CUDA(cudaMemcpy(deg, dd.p, count * 8, cudaMemcpyDeviceToHost));
+    return HBFS_OK;
+    HB_ENTRY_END
+}
+
+// Exchange volume of the last hbfs_mg_bfs / hbfs_mgl_bfs traversal of this
+// part: out[0] records sent (8 bytes each), out[1] records received, out[2]
+// layers (one next-frontier all-gather and one counter all-reduce each),
+// out[3] top-down record exchanges.
+extern "C" int hbfs_part_exchange_stats(const hbfs_part *P, int64_t *out) {
+    HB_ENTRY_BEGIN
+    if (!P || !out) return set_error(HBFS_EINVAL, "bad arguments");
+    for (int k = 0; k < 4; ++k) out[k] = P->stat[k];
     return HBFS_OK;
     HB_ENTRY_END
 }
@@ -956,7 +996,8 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
             P->cap_r = n + 1;
         }
         if (!P->acnt.p) HB_CHECK(P->acnt.alloc(64));
-        if (!P->h_acnt && cudaMallocHost(&P->h_acnt, 16) != cudaSuccess)
+        if (!P->lay.p) HB_CHECK(P->lay.alloc(64));
+        if (!P->h_acnt && cudaMallocHost(&P->h_acnt, 32) != cudaSuccess)
             return set_error(HBFS_ECUDA, "cudaMallocHost failed");
         if (!P->counts_dev.p) HB_CHECK(P->counts_dev.alloc(16 * world + 16));
     }
@@ -965,20 +1006,22 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
     HB_CUDA(cudaEventCreate(&ev1));
     HB_CUDA(cudaEventRecord(ev0, st));
     // root degree and global arc count
-    int64_t h2[2] = {0, 0};
+    int64_t h2[3] = {0, 0, 0};  // root degree, arcs, vertices with degree > 0
     for (int i = 0; i < nparts; ++i) {
         int64_t d = 0;
         if (root >= Ps[i]->lo && root < Ps[i]->hi) HB_CHECK(hbfs_part_degree(Ps[i], root, &d));
         h2[0] += d;
         h2[1] += Ps[i]->arcs;
+        h2[2] += Ps[i]->n_pos;
     }
-    if (M) {
+    if (M && world > 1) {
         int64_t *scal = M->scal.as<int64_t>();
-        HB_CUDA(cudaMemcpyAsync(scal, h2, 16, cudaMemcpyHostToDevice, st));
-        HB_NCCL(nccl().allReduce(scal, scal, 2, ncclInt64, ncclSum, M->comm, st));
-        HB_CUDA(cudaMemcpyAsync(h2, scal, 16, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(scal, h2, 24, cudaMemcpyHostToDevice, st));
+        HB_NCCL(nccl().allReduce(scal, scal, 3, ncclInt64, ncclSum, M->comm, st));
+        HB_CUDA(cudaMemcpyAsync(h2, scal, 24, cudaMemcpyDeviceToHost, st));
         HB_CUDA(cudaStreamSynchronize(st));
     }
+    const int64_t n_pos = h2[2], ratio = bu_exec_ratio();
     Heur H;
     H.heuristic = p->heuristic;
     H.counter_mode = p->counter_mode;
@@ -990,24 +1033,23 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
     int cur = HBFS_TOP_DOWN;
     std::vector<int64_t> hc((size_t)2 * world * nparts);  // [part][send world | recv world]
     auto t_layer = std::chrono::steady_clock::now();
+    for (int i = 0; i < nparts; ++i) Ps[i]->stat[0] = Ps[i]->stat[1] = Ps[i]->stat[2] = Ps[i]->stat[3] = 0;
     while (v_f > 0) {
         int64_t fv, gv;
         const int d = decide(H, cur, v_f, e_f, eu_v, eu_e, prev_vf, &fv, &gv);
         const int64_t state[6] = {layer, v_f, e_f, eu_v, eu_e, prev_vf};
-        unsigned long long tot[4] = {0, 0, 0, 0};
-        for (int i = 0; i < nparts; ++i)  // asynchronous; counters read after the next sync
-            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, st));
-        bool have_ctr = false;
-        auto add_trav_counters = [&]() {
-            if (have_ctr) return;
-            for (int i = 0; i < nparts; ++i) {
-                unsigned long long c[4];
-                part_trav_counters(Ps[i]->trav, c);
-                for (int k = 0; k < 4; ++k) tot[k] += c[k];
-            }
-            have_ctr = true;
-        };
-        if (d == HBFS_TOP_DOWN) {
+        // The layer's counter totals are summed on the device (this process's
+        // parts, then all-reduced over the ranks) and read back with the one
+        // stream synchronisation that ends the layer; a top-down layer of a
+        // partition with more than one rank needs one more, for the record
+        // counts NCCL takes from the host.
+        unsigned long long *lay = P0->lay.as<unsigned long long>();
+        HB_CUDA(cudaMemsetAsync(lay, 0, 32, st));
+        for (int i = 0; i < nparts; ++i)  // asynchronous
+            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, n_pos, st));
+        // records only after a real top-down expansion with remote targets
+        const bool exchange = d == HBFS_TOP_DOWN && world > 1 && !bu_executes(d, 1, eu_v, e_f, n, n_pos, ratio);
+        if (exchange) {
             for (int i = 0; i < nparts; ++i)
                 HB_CHECK(td_owner_counts(Ps[i], world, wper, Ps[i]->counts_dev.as<int64_t>(), st));
             if (M) {
@@ -1025,7 +1067,6 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                             cudaMemcpyDeviceToHost, st));
             }
             HB_CUDA(cudaStreamSynchronize(st));
-            add_trav_counters();
             if (!M)  // recv[i][s] = send[s][i]
                 for (int i = 0; i < nparts; ++i)
                     for (int sr = 0; sr < world; ++sr) hc[(size_t)2 * world * i + world + sr] = hc[(size_t)2 * world * sr + i];
@@ -1036,6 +1077,9 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                     ns += hc[(size_t)2 * world * i + r];
                     nr += hc[(size_t)2 * world * i + world + r];
                 }
+                P->stat[0] += ns;
+                P->stat[1] += nr;
+                P->stat[3] += 1;
                 if ((size_t)ns + 1 > P->cap_s) {
                     HB_CHECK(P->recs_s.alloc((ns + ns / 4 + 1024) * 8));
                     P->cap_s = ns + ns / 4 + 1024;
@@ -1085,14 +1129,18 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                                                P->parent.as<uint32_t>(), P->level.as<int32_t>(),
                                                                part_trav_plane(P->trav, layer + 1),
                                                                P->acnt.as<unsigned long long>());
-                HB_CUDA(cudaMemcpyAsync(P->h_acnt, P->acnt.p, 16, cudaMemcpyDeviceToHost, st));
             }
         }
+        for (int i = 0; i < nparts; ++i)
+            HB_CHECK(part_trav_add_counters(Ps[i]->trav, layer, exchange ? Ps[i]->acnt.as<unsigned long long>() : nullptr,
+                                            lay, st));
         // next frontier: every rank's owned words of plane layer+1 to everyone
-        if (M) {
+        // (the next launch ORs the all-gathered plane into the visited bitmap)
+        if (M && world > 1) {
             uint32_t *pl = part_trav_plane(Ps[0]->trav, layer + 1);
             HB_NCCL(nccl().allGather(pl + M->rank * wper, pl, (size_t)wper, ncclUint32, M->comm, st));
-        } else {
+            HB_NCCL(nccl().allReduce(lay, lay, 4, ncclUint64, ncclSum, M->comm, st));
+        } else if (!M) {
             for (int i = 0; i < nparts; ++i)
                 for (int sr = 0; sr < nparts; ++sr)
                     if (sr != i)
@@ -1100,21 +1148,9 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                                 part_trav_plane(Ps[sr]->trav, layer + 1) + sr * wper, wper * 4,
                                                 cudaMemcpyDeviceToDevice, st));
         }
-        // (the next launch ORs the all-gathered plane into the visited bitmap)
+        HB_CUDA(cudaMemcpyAsync(P0->h_acnt, lay, 32, cudaMemcpyDeviceToHost, st));
         HB_CUDA(cudaStreamSynchronize(st));
-        add_trav_counters();
-        if (d == HBFS_TOP_DOWN)
-            for (int i = 0; i < nparts; ++i) {
-                tot[0] += Ps[i]->h_acnt[0];
-                tot[1] += Ps[i]->h_acnt[1];
-            }
-        if (M) {
-            unsigned long long *ctr = M->ctr.as<unsigned long long>();
-            HB_CUDA(cudaMemcpyAsync(ctr, tot, 32, cudaMemcpyHostToDevice, st));
-            HB_NCCL(nccl().allReduce(ctr, ctr, 4, ncclUint64, ncclSum, M->comm, st));
-            HB_CUDA(cudaMemcpyAsync(tot, ctr, 32, cudaMemcpyDeviceToHost, st));
-            HB_CUDA(cudaStreamSynchronize(st));
-        }
+        const unsigned long long *tot = P0->h_acnt;
         if (trace && layer < trace_cap) {
             hbfs_layer_row &r = trace[layer];
             r.layer = (int32_t)(layer + 1);
@@ -1130,6 +1166,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
             r.elapsed = std::chrono::duration<double>(now - t_layer).count();  // host wall of the layer
             t_layer = now;
         }
+        for (int i = 0; i < nparts; ++i) Ps[i]->stat[2] += 1;
         prev_vf = v_f;
         v_f = (int64_t)tot[0];
         e_f = (int64_t)tot[1];

@@ -222,6 +222,7 @@ class CudaRankOps:
         _lib.check(lib.hbfs_part_build(C.c_void_p(u.data_ptr()), C.c_void_p(v.data_ptr()), m, n, lo,
                                        hi, int(dedup), 1, None, C.byref(h)))
         del u, v
+        torch.cuda.empty_cache()  # libhbfs allocates with cudaMalloc: hand the edge list's memory back
         return cls(h, dev)
 
     @classmethod
@@ -284,17 +285,75 @@ class CudaRankOps:
     def absorb(self, next_full):
         self._lib.check(self.lib.hbfs_part_absorb(self.h, C.c_void_p(next_full.data_ptr()), self._s()))
 
+    def degrees(self, ids) -> np.ndarray:
+        """Degrees of the listed vertices this rank owns (0 for the others)."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        deg = np.zeros(len(ids), dtype=np.int64)
+        self._lib.check(self.lib.hbfs_part_degrees(self.h, ids.ctypes.data_as(C.c_void_p), len(ids),
+                                                   deg.ctypes.data_as(C.c_void_p)))
+        return deg
+
+    def exchange_stats(self) -> dict:
+        """Exchange volume of the last traversal through the C++ loop."""
+        out = (C.c_int64 * 4)()
+        self._lib.check(self.lib.hbfs_part_exchange_stats(self.h, out))
+        return {"records_sent": out[0], "records_received": out[1], "layers": out[2], "record_exchanges": out[3]}
+
     def outputs(self):
-        par = np.empty(self.nloc, dtype=np.uint32)
-        lev = np.empty(self.nloc, dtype=np.int32)
-        self._lib.check(self.lib.hbfs_part_outputs(self.h, par.ctypes.data_as(C.c_void_p),
-                                                   lev.ctypes.data_as(C.c_void_p), 0, self._s()))
-        return par, lev
+        """Owned parent/level slices on the host, in pinned arrays reused by
+        the next call (the copy runs at the PCIe rate, not through the
+        driver's pageable staging)."""
+        import torch
+
+        if getattr(self, "_out", None) is None:
+            self._out = (torch.empty(max(self.nloc, 1), dtype=torch.int32, pin_memory=True),
+                         torch.empty(max(self.nloc, 1), dtype=torch.int32, pin_memory=True))
+        tp, tl = self._out
+        self._lib.check(self.lib.hbfs_part_outputs(self.h, C.c_void_p(tp.data_ptr()), C.c_void_p(tl.data_ptr()),
+                                                   0, self._s()))
+        torch.cuda.current_stream().synchronize()
+        return tp.numpy()[: self.nloc].view(np.uint32), tl.numpy()[: self.nloc]
 
     def new_tensor(self, size, dtype_name):
         import torch
 
         return torch.empty(size, dtype=getattr(torch, dtype_name), device=self.device)
+
+
+def sample_sources_partitioned(ranks, comm, count: int, seed: int) -> np.ndarray:
+    """harness.sample_sources (harness.py:73-97) for a partitioned graph: the
+    sampling order does not depend on the graph, so its head is generated
+    alone (hbfs_source_order_prefix) and filtered by the degrees the ranks
+    hold (summed over ranks) — no rank builds the whole CSR.  `ranks`: the
+    CudaRankOps this process owns; `comm`: LocalComm / TorchComm."""
+    from . import _lib
+
+    lib = _lib.load(require_device=True)
+    r0 = ranks[0]
+    n = r0.n
+    want = min(n, max(4 * count, 1024))
+    while True:
+        ids = np.empty(want, dtype=np.uint32)
+        _lib.check(lib.hbfs_source_order_prefix(n, seed & 0xFFFFFFFFFFFFFFFF, want, ids.ctypes.data_as(C.c_void_p)))
+        bufs = []
+        for r in ranks:
+            t = r.new_tensor(want, "int64")
+            t.copy_(_torch_from(r.degrees(ids)))
+            bufs.append(t)
+        comm.all_reduce_sum(bufs)
+        deg = bufs[0].cpu().numpy()
+        sel = ids[deg > 0][:count]
+        if len(sel) == count:
+            return sel
+        if want >= n:
+            raise ValueError(f"only {len(sel)} vertices with degree >= 1, need {count}")
+        want = min(n, want * 4)
+
+
+def _torch_from(a):
+    import torch
+
+    return torch.from_numpy(a)
 
 
 # ------------------------------------------------------------- controller
