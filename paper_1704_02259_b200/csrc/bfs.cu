@@ -1761,6 +1761,8 @@ static const Variant<OffT> *variants(int *count) {
         {(const void *)bfs_kernel<OffT, 1, 2, true>, 1, 2},
         {(const void *)bfs_kernel<OffT, 2, 2, true>, 2, 2},
         {(const void *)bfs_kernel<OffT, 4, 1, false>, 4, 1},
+        {(const void *)bfs_kernel<OffT, 3, 2, true>, 3, 2},
+        {(const void *)bfs_kernel<OffT, 4, 2, true>, 4, 2},
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
@@ -1768,13 +1770,14 @@ static const Variant<OffT> *variants(int *count) {
 constexpr int kDefaultVariant = 0;
 
 // Measured on B200 (tools/diag.py sweeps): small graphs are latency-bound and
-// prefer one fat CTA per SM with 4 searches in flight per lane (variant 4);
-// SCALE >= 24 prefers two CTAs per SM with 2 searches per lane (variant 3).
+// prefer one fat CTA per SM with 4 head records in flight per lane (variant 4);
+// SCALE >= 24 prefers two CTAs per SM with 3 per lane (variant 5; S26, 32
+// roots: 2 per lane 1041, 3: 1060, 4: 1046 GTEPS).
 
 static int variant_index(int64_t n) {
     const char *e = getenv("HBFS_KERNEL_VARIANT");
     if (e) return atoi(e);
-    return n >= (int64_t(1) << 24) ? 3 : 4;
+    return n >= (int64_t(1) << 24) ? 5 : 4;
 }
 
 // ------------------------------------------------------------ workspace
