@@ -15,6 +15,15 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
+
+
+def int(x, _int=int):  # reports with several launches repeat the header rows
+    try:
+        return _int(x)
+    except (TypeError, ValueError):
+        return 0
+
+
 ih = hdr.index("L2 Explicit Hit Policy Evict Normal")
 im = hdr.index("L2 Explicit Miss Policy Evict Normal")
 ie = hdr.index("Instructions Executed")
