@@ -370,6 +370,19 @@ __device__ __forceinline__ uint4 ld_adj4(const uint32_t *p) {
     return r;
 }
 
+// Row start with the 64-byte L2 fetch hint (a lone 4- or 8-byte read of a line).
+template <typename OffT>
+__device__ __forceinline__ OffT ld_rs(const OffT *p) {
+    if (sizeof(OffT) == 4) {
+        uint32_t r;
+        asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(r) : "l"(p));
+        return (OffT)r;
+    }
+    unsigned long long r;
+    asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(p));
+    return (OffT)r;
+}
+
 // Opaque global-space copy of a pointer: the compiler cannot rematerialise it (it would
 // otherwise rebuild the bitmap plane address from the parameter bank with a
 // 64-bit add chain at every probe — 5 extra instructions per probe).
@@ -944,7 +957,7 @@ __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, c
     if (act) {
         ent.y = __ldg(&A.hd[slot].x);
         HB_DCHECK(ent.x < A.n, 6);
-        r0 = __ldg(A.rs + ent.x);
+        r0 = PF ? ld_rs<OffT>(A.rs + ent.x) : __ldg(A.rs + ent.x);
         HB_DCHECK((int64_t)r0 + ent.y <= A.arcs, 4);
     }
     const OffT s = (OffT)(r0 + kHeadLen), e = (OffT)(r0 + ent.y);
@@ -1611,7 +1624,9 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             BuSmem &bs = *reinterpret_cast<BuSmem *>(dsm);  // the top-down staging area is idle
             // rows walked per lane before the cooperative scan: 2 vectors, 4 behind
             // a small frontier (there most open rows are scanned to their end)
-            phase_bu<OffT, K, PART>(A, S, in, out, spare, ctr, red, sf, bs,
+            // (large graphs: an open row's vector that misses L2 fetches 64 bytes, not
+            // the 128-byte line — tools/mb/sector.cu — most rows stop within it)
+            phase_bu<OffT, K, PART, SCAN ? 64 : 0>(A, S, in, out, spare, ctr, red, sf, bs,
                                     SCAN && S.v_f * 64 < A.n ? kLaneVecsScan : kLaneVecs);
         }
         grid.sync();
