@@ -46,6 +46,12 @@ class CpuRankOps:
             return int(self.rs[v - self.lo + 1] - self.rs[v - self.lo])
         return 0
 
+    def degrees(self, ids) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        own = (ids >= self.lo) & (ids < self.hi)
+        loc = np.where(own, ids - self.lo, 0)
+        return np.where(own, self.rs[loc + 1] - self.rs[loc], 0).astype(np.int64)
+
     def init(self, root: int):
         self.parent = np.full(self.nloc, NIL, dtype=np.uint32)
         self.level = np.full(self.nloc, -1, dtype=np.int32)

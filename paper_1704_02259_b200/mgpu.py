@@ -320,21 +320,29 @@ class CudaRankOps:
         return torch.empty(size, dtype=getattr(torch, dtype_name), device=self.device)
 
 
-def sample_sources_partitioned(ranks, comm, count: int, seed: int) -> np.ndarray:
+def sample_sources_partitioned(ranks, comm, count: int, seed: int, order_prefix=None) -> np.ndarray:
     """harness.sample_sources (harness.py:73-97) for a partitioned graph: the
     sampling order does not depend on the graph, so its head is generated
     alone (hbfs_source_order_prefix) and filtered by the degrees the ranks
     hold (summed over ranks) — no rank builds the whole CSR.  `ranks`: the
-    CudaRankOps this process owns; `comm`: LocalComm / TorchComm."""
-    from . import _lib
+    rank objects this process owns; `comm`: LocalComm / TorchComm;
+    `order_prefix(n, seed, k)` (tests: a CPU restatement) defaults to the
+    device routine."""
+    if order_prefix is None:
+        from . import _lib
 
-    lib = _lib.load(require_device=True)
+        lib = _lib.load(require_device=True)
+
+        def order_prefix(n, seed, k):
+            ids = np.empty(k, dtype=np.uint32)
+            _lib.check(lib.hbfs_source_order_prefix(n, seed & 0xFFFFFFFFFFFFFFFF, k, ids.ctypes.data_as(C.c_void_p)))
+            return ids
+
     r0 = ranks[0]
     n = r0.n
     want = min(n, max(4 * count, 1024))
     while True:
-        ids = np.empty(want, dtype=np.uint32)
-        _lib.check(lib.hbfs_source_order_prefix(n, seed & 0xFFFFFFFFFFFFFFFF, want, ids.ctypes.data_as(C.c_void_p)))
+        ids = np.ascontiguousarray(order_prefix(n, seed, want), dtype=np.uint32)
         bufs = []
         for r in ranks:
             t = r.new_tensor(want, "int64")

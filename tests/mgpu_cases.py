@@ -29,7 +29,7 @@ def worker(rank: int, world: int, port: int, outdir: str, backend: str = "gloo")
     from oracle import oracle as O
     from oracle.part_cpu import CpuRankOps
     from paper_1704_02259_b200.hybrid import HeuristicParams
-    from paper_1704_02259_b200.mgpu import DistBfs, TorchComm
+    from paper_1704_02259_b200.mgpu import DistBfs, TorchComm, sample_sources_partitioned
 
     out = {}
     for ci, (scale, ef, seed, probs, hk, force) in enumerate(CASES):
@@ -37,6 +37,10 @@ def worker(rank: int, world: int, port: int, outdir: str, backend: str = "gloo")
         host = O.csr_build(u, v, 1 << scale)
         ops = CpuRankOps(host.row_starts, host.adjacency, host.in_edges_total, world, rank)
         db = DistBfs([ops], TorchComm())
+        # root sampling without any rank holding all degrees (the order prefix
+        # from the oracle: the sampling order with isolated vertices allowed)
+        out[f"{ci}/sources"] = sample_sources_partitioned(
+            [ops], TorchComm(), 16, 5, order_prefix=lambda n, seed, k: O.sample_sources(host, k, seed, allow_isolated=True))
         for ri, root in enumerate(O.sample_sources(host, 3, 1)):
             res = db.bfs(int(root), HeuristicParams(**hk), use_simd=True, force_direction=force)
             par, lev = db.outputs()[0]

@@ -37,6 +37,8 @@ def test_partitioned_controller_matches_reference(world, tmp_path, oracle):
         u, v = oracle.generate(scale, ef, seed, probs)
         host = oracle.csr_build(u, v, 1 << scale)
         p = HeuristicParams(**hk)
+        for pp in parts:  # partitioned root sampling = the reference's, on every rank
+            assert np.array_equal(pp[f"{ci}/sources"], oracle.sample_sources(host, 16, 5)), ci
         for ri, root in enumerate(oracle.sample_sources(host, 3, 1)):
             par = np.concatenate([pp[f"{ci}/{ri}/parent"] for pp in parts])
             lev = np.concatenate([pp[f"{ci}/{ri}/level"] for pp in parts])
