@@ -109,6 +109,7 @@ struct Args {
     const uint32_t *posw;
     const uint4 *hd;      // head records (common.cuh), rank order over the degree > 0 vertices
     const uint32_t *pre;  // records before bitmap word w (indexed like posw)
+    const uint4 *hd2;     // second-tier records (common.cuh), two uint4 per slot
     int64_t n, nw, arcs, ncs;
     int64_t n_pos;        // vertices with degree > 0 (head records)
     uint32_t *parent;
@@ -397,15 +398,19 @@ __device__ __forceinline__ const uint32_t *pin_ptr(const uint32_t *p) {
 struct Probe {
     const uint32_t *bm;  // frontier plane (global-space address, pin_ptr)
     __device__ __forceinline__ uint32_t word(uint32_t a) const { return probe_word(bm, a); }
-    // 4 entries of a row vector: bit j of the result = val[j] is in the frontier
-    __device__ __forceinline__ uint32_t hits4(const uint32_t (&val)[4], const bool (&ok)[4]) const {
-        uint32_t w[4];
+    // N row entries: bit j of the result = val[j] is in the frontier
+    template <int N>
+    __device__ __forceinline__ uint32_t hitsn(const uint32_t (&val)[N], const bool (&ok)[N]) const {
+        uint32_t w[N];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = ok[j] ? word(val[j]) : 0u;
+        for (int j = 0; j < N; ++j) w[j] = ok[j] ? word(val[j]) : 0u;
         uint32_t hm = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) hm |= ((w[j] >> (val[j] & 31)) & 1u) << j;
+        for (int j = 0; j < N; ++j) hm |= ((w[j] >> (val[j] & 31)) & 1u) << j;
         return hm;
+    }
+    __device__ __forceinline__ uint32_t hits4(const uint32_t (&val)[4], const bool (&ok)[4]) const {
+        return hitsn<4>(val, ok);
     }
 };
 
@@ -940,39 +945,72 @@ struct BuCount {
 };
 
 // Drain up to 32 open candidates from the top of the warp's list: lane i
-// continues row i at position kHeadLen (its degree is re-read from the head
-// record, a cache hit).
+// continues row i at position kHeadLen — first in its second-tier record (one
+// 32-byte sector: row start + the next 7 entries, 6 with 64-bit offsets), then,
+// if the row is longer and still open, in the CSR row itself.
 template <typename OffT, int PF>
 __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, const uint16_t *ol,
                                          uint32_t &nopen, int64_t tw, uint32_t prel, uint32_t *s_found,
                                          int64_t max_pos, int32_t depth1, int lv, BuCount &cnt) {
+    constexpr int RW = sizeof(OffT) / 4, NE = 8 - RW;  // second-tier record: row start, then NE entries
     const int lane = threadIdx.x & 31;
     const uint32_t take = nopen < 32u ? nopen : 32u;
     nopen -= take;
     const bool act = (uint32_t)lane < take;
     const uint32_t oe = act ? ol[nopen + lane] : 0u;
     const uint32_t slot = __shfl_sync(0xffffffffu, prel, (oe >> 5) & 31) + (oe >> 10);
-    uint2 ent = make_uint2((uint32_t)(tw * 32) + (oe & 1023u), 0u);  // vertex, degree
-    OffT r0 = 0;
+    const uint32_t v = (uint32_t)(tw * 32) + (oe & 1023u);
+    uint32_t deg = 0;
+    uint4 ra = make_uint4(0, 0, 0, 0), rb = make_uint4(0, 0, 0, 0);
     if (act) {
-        ent.y = __ldg(&A.hd[slot].x);
-        HB_DCHECK(ent.x < A.n, 6);
-        r0 = PF ? ld_rs<OffT>(A.rs + ent.x) : __ldg(A.rs + ent.x);
-        HB_DCHECK((int64_t)r0 + ent.y <= A.arcs, 4);
+        HB_DCHECK(v < A.n, 6);
+        deg = __ldg(&A.hd[slot].x);  // a cache hit: the head phase just read the record
+        ra = __ldg(A.hd2 + 2 * (int64_t)slot);
+        rb = __ldg(A.hd2 + 2 * (int64_t)slot + 1);
     }
-    const OffT s = (OffT)(r0 + kHeadLen), e = (OffT)(r0 + ent.y);
-    int64_t hit;
-    uint32_t hu;
-    first_hits<OffT, PF>(A.adj, bm, act, s, e, lv, hit, hu);
+    const uint32_t w[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+    const OffT r0 = RW == 2 ? (OffT)(((uint64_t)w[1] << 32) | w[0]) : (OffT)w[0];
+    HB_DCHECK(!act || (int64_t)r0 + deg <= A.arcs, 4);
+    // the record's entries: row positions kHeadLen .. kHeadLen + NE - 1
+    uint32_t val[NE];
+    bool ok[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+        val[j] = w[RW + j];
+        ok[j] = act && (uint32_t)(kHeadLen + j) < deg;
+    }
+    const uint32_t hm = bm.template hitsn<NE>(val, ok);
+    int64_t hit = -1;
+    uint32_t hu = 0;
+    if (hm) {
+        const int j = __ffs(hm) - 1;
+        hit = (int64_t)r0 + kHeadLen + j;
+        hu = val[0];  // selects, not val[j]: a dynamic index would put val[] in local memory
+#pragma unroll
+        for (int i = 1; i < NE; ++i)
+            if (j == i) hu = val[i];
+    }
+    // rows longer than both records that are still open continue in the CSR row
+    const bool deep = act && !hm && deg > (uint32_t)(kHeadLen + NE);
+    if (__any_sync(0xffffffffu, deep)) {
+        const OffT s = (OffT)(r0 + kHeadLen + NE), e = (OffT)(r0 + deg);
+        int64_t hit2;
+        uint32_t hu2;
+        first_hits<OffT, PF>(A.adj, bm, deep, s, e, lv, hit2, hu2);
+        if (deep) {
+            hit = hit2;
+            hu = hu2;
+        }
+    }
     if (act) {
         const bool found = hit >= 0;
         if (found) {
-            HB_DCHECK(hu < A.n && hit < (int64_t)e && hit >= (int64_t)s, 0);
-            A.parent[ent.x] = hu;
-            if (A.direct_levels) A.level[ent.x] = depth1;
-            atomicOr(&s_found[(ent.x >> 5) - tw], 1u << (ent.x & 31));
+            HB_DCHECK(hu < A.n && hit < (int64_t)r0 + deg && hit >= (int64_t)r0 + kHeadLen, 0);
+            A.parent[v] = hu;
+            if (A.direct_levels) A.level[v] = depth1;
+            atomicOr(&s_found[(v >> 5) - tw], 1u << (v & 31));
         }
-        cnt.add(found, found ? hit - (int64_t)r0 : -1, (int64_t)ent.y, max_pos);
+        cnt.add(found, found ? hit - (int64_t)r0 : -1, (int64_t)deg, max_pos);
     }
     __syncwarp();  // the list slots just read may be pushed over
 }
@@ -1710,7 +1748,7 @@ __global__ void part_bu_counters(const Ctr *c, unsigned long long *out) {
 size_t part_bu_scratch_bytes() { return sizeof(Ctl) + 64; }
 
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local,
-                   const uint4 *hd_local, const uint32_t *pre_local, int64_t n,
+                   const uint4 *hd_local, int64_t n_pos_local, const uint32_t *pre_local, int64_t n,
                    int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st) {
@@ -1722,6 +1760,7 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
     A.adj = adj;
     A.posw = posw_local - wlo;
     A.hd = hd_local;  // rank order within the partition
+    A.hd2 = hd_local + head2_offset(n_pos_local);
     A.pre = pre_local - (lo >> 5);
     A.n = n;
     A.nw = (n + 31) / 32;
@@ -1909,6 +1948,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.adj = g->adj.as<uint32_t>();
     A.posw = g->posw.as<uint32_t>();
     A.hd = g->hd.as<uint4>();
+    A.hd2 = g->hd.as<uint4>() + head2_offset(g->n_pos);
     A.pre = g->pre.as<uint32_t>();
     A.n_pos = g->n_pos;
     A.bu_exec_ratio = bu_exec_ratio();
@@ -2039,7 +2079,7 @@ static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 
 
 void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
                        const uint32_t *adj, const uint32_t *posw_local, const uint4 *hd_local,
-                       const uint32_t *pre_local, uint32_t *parent_local,
+                       int64_t n_pos_local, const uint32_t *pre_local, uint32_t *parent_local,
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad) {
     PartTrav *T = new PartTrav();
     // planes padded to world * (words per rank): the in-place all-gather of a
@@ -2088,6 +2128,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.adj = adj;
     A.posw = posw_local - (lo >> 5);
     A.hd = hd_local;  // rank order within the partition
+    A.hd2 = hd_local + head2_offset(n_pos_local);
     A.pre = pre_local - (lo >> 5);
     A.n = n;
     A.nw = nw;

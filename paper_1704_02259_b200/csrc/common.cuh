@@ -147,6 +147,16 @@ __host__ __device__ inline int decide(const Heur &H, int cur, int64_t v_f, int64
 // candidates of a dense layer read them as contiguous runs.  Built once per
 // graph (graph_finalize / part build); synchronises the stream.
 constexpr int kHeadLen = 3;
+// Second-tier record (32 bytes = one sector, same slot as the head record, stored
+// behind the head records in the same buffer at head2_offset): the row start
+// and the next row entries — positions kHeadLen .. kHeadLen + 6 with 32-bit
+// row offsets (word 0 = row start), kHeadLen .. kHeadLen + 5 with 64-bit ones
+// (words 0-1).  A candidate its head record left open continues here: one
+// sector instead of the row-start sector plus the row's first adjacency
+// sectors, and no dependent row-start load in front of the row.
+__host__ __device__ inline int64_t head2_offset(int64_t n_records) {  // in uint4 units, sector-aligned
+    return (n_records + 2) & ~int64_t(1);
+}
 int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
                 DevBuf &pre, DevBuf &hd, cudaStream_t st, int64_t *n_records = nullptr);
 
@@ -168,7 +178,7 @@ int64_t bu_exec_ratio();  // HBFS_BU_EXEC_RATIO or the default
 // (< 0: unknown).  scratch: part_bu_scratch_bytes() of device memory.
 size_t part_bu_scratch_bytes();
 int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t *posw_local,
-                   const uint4 *hd_local, const uint32_t *pre_local, int64_t n,
+                   const uint4 *hd_local, int64_t n_pos_local, const uint32_t *pre_local, int64_t n,
                    int64_t lo, int64_t nloc, int64_t arcs_local, const uint32_t *F, uint32_t *V, uint32_t *parent_local,
                    int32_t *level_local, uint32_t *next_slice, int32_t depth, int32_t max_pos, int64_t v_f,
                    unsigned long long *counters, void *scratch, cudaStream_t st);
@@ -177,7 +187,7 @@ int part_bu_launch(const uint64_t *rs_local, const uint32_t *adj, const uint32_t
 // (bfs.cu; driven by the multi-GPU loop in part.cu).
 void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, const uint64_t *rs_local,
                        const uint32_t *adj, const uint32_t *posw_local, const uint4 *hd_local,
-                       const uint32_t *pre_local, uint32_t *parent_local,
+                       int64_t n_pos_local, const uint32_t *pre_local, uint32_t *parent_local,
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad);
 void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap

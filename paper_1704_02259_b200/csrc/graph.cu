@@ -208,7 +208,8 @@ struct PopcOp {
 
 template <typename OffT>
 __global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, const uint32_t *posw,
-                        const uint32_t *pre, uint4 *hd) {
+                        const uint32_t *pre, uint4 *hd, uint4 *hd2) {
+    constexpr int RW = sizeof(OffT) / 4;  // words of the row start in the second-tier record
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         const OffT s = rs[v];
@@ -219,7 +220,18 @@ __global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, const ui
         h.y = adj[(uint64_t)s];
         h.z = d > 1 ? adj[(uint64_t)s + 1] : HBFS_NIL;
         h.w = d > 2 ? adj[(uint64_t)s + 2] : HBFS_NIL;
-        hd[pre[v >> 5] + __popc(posw[v >> 5] & ((1u << (v & 31)) - 1u))] = h;
+        const int64_t slot = pre[v >> 5] + __popc(posw[v >> 5] & ((1u << (v & 31)) - 1u));
+        hd[slot] = h;
+        uint32_t w[8];
+        w[0] = (uint32_t)((uint64_t)s & 0xFFFFFFFFu);
+        if (RW == 2) w[1] = (uint32_t)((uint64_t)s >> 32);
+#pragma unroll
+        for (int j = RW; j < 8; ++j) {
+            const uint64_t pos = (uint64_t)kHeadLen + (j - RW);
+            w[j] = pos < d ? adj[(uint64_t)s + pos] : HBFS_NIL;
+        }
+        hd2[2 * slot] = make_uint4(w[0], w[1], w[2], w[3]);
+        hd2[2 * slot + 1] = make_uint4(w[4], w[5], w[6], w[7]);
     }
 }
 
@@ -242,15 +254,16 @@ int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const 
         HB_CUDA(cudaStreamSynchronize(st));
     }
     if (n_records) *n_records = (int64_t)total;
-    HB_CHECK(hd.alloc(((size_t)total + 1) * sizeof(uint4)));
+    const int64_t off2 = head2_offset((int64_t)total);
+    HB_CHECK(hd.alloc(((size_t)off2 + 2 * ((size_t)total + 1)) * sizeof(uint4)));
     if (n <= 0) return HBFS_OK;
     const int blocks = grid_for(n);
     if (wide)
         k_heads<uint64_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint64_t *>(rs), adj, posw,
-                                                 pre.as<uint32_t>(), hd.as<uint4>());
+                                                 pre.as<uint32_t>(), hd.as<uint4>(), hd.as<uint4>() + off2);
     else
         k_heads<uint32_t><<<blocks, 256, 0, st>>>(n, static_cast<const uint32_t *>(rs), adj, posw,
-                                                 pre.as<uint32_t>(), hd.as<uint4>());
+                                                 pre.as<uint32_t>(), hd.as<uint4>(), hd.as<uint4>() + off2);
     HB_CUDA(cudaGetLastError());
     HB_CUDA(cudaStreamSynchronize(st));
     return HBFS_OK;

@@ -694,7 +694,7 @@ extern "C" int hbfs_part_bu(hbfs_part *P, int32_t depth, int32_t max_pos, uint32
     if (!P || !next_slice || !counters) return set_error(HBFS_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the persistent kernel's bottom-up tiles on the owned words (bfs.cu)
-    HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->pre.as<uint32_t>(), P->n, P->lo,
+    HB_CHECK(part_bu_launch(P->rs.as<uint64_t>(), P->adj.as<uint32_t>(), P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->n_pos, P->pre.as<uint32_t>(), P->n, P->lo,
                             P->nloc, P->arcs, P->F.as<uint32_t>(), P->V.as<uint32_t>(), P->parent.as<uint32_t>(),
                             P->level.as<int32_t>(), next_slice, depth, max_pos, P->fhint, counters,
                             P->bu_scratch.p, st));
@@ -978,7 +978,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
         if (!P->trav) {
             int rc = HBFS_OK;
             P->trav = part_trav_create(n, P->lo, P->nloc, P->arcs, P->rs.as<uint64_t>(), P->adj.as<uint32_t>(),
-                                       P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->pre.as<uint32_t>(), P->parent.as<uint32_t>(),
+                                       P->posw.as<uint32_t>(), P->hd.as<uint4>(), P->n_pos, P->pre.as<uint32_t>(), P->parent.as<uint32_t>(),
                                        P->level.as<int32_t>(),
                                        reinterpret_cast<uint32_t *>(P->cand.as<int32_t>()), P->touch.as<uint32_t>(),
                                        &rc, nw_pad);
