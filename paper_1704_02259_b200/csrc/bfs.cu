@@ -952,7 +952,7 @@ template <typename OffT, int PF>
 __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, const uint16_t *ol,
                                          uint32_t &nopen, int64_t tw, uint32_t prel, uint32_t *s_found,
                                          int64_t max_pos, int32_t depth1, int lv, BuCount &cnt) {
-    constexpr int RW = sizeof(OffT) / 4, NE = 8 - RW;  // second-tier record: row start, then NE entries
+    constexpr int RW = sizeof(OffT) / 4, NE = kH2W - RW;  // second-tier record: row start, then NE entries
     const int lane = threadIdx.x & 31;
     const uint32_t take = nopen < 32u ? nopen : 32u;
     nopen -= take;
@@ -961,14 +961,22 @@ __device__ __forceinline__ void bu_drain(const Args<OffT> &A, const Probe &bm, c
     const uint32_t slot = __shfl_sync(0xffffffffu, prel, (oe >> 5) & 31) + (oe >> 10);
     const uint32_t v = (uint32_t)(tw * 32) + (oe & 1023u);
     uint32_t deg = 0;
-    uint4 ra = make_uint4(0, 0, 0, 0), rb = make_uint4(0, 0, 0, 0);
+    uint32_t w[kH2W];
+#pragma unroll
+    for (int j = 0; j < kH2W; ++j) w[j] = 0;
     if (act) {
         HB_DCHECK(v < A.n, 6);
         deg = __ldg(&A.hd[slot].x);  // a cache hit: the head phase just read the record
-        ra = __ldg(A.hd2 + 2 * (int64_t)slot);
-        rb = __ldg(A.hd2 + 2 * (int64_t)slot + 1);
+        const uint32_t *r2 = reinterpret_cast<const uint32_t *>(A.hd2 + (kH2W / 4) * (int64_t)slot);
+#pragma unroll
+        for (int q = 0; q < kH2W / 4; ++q) {
+            const uint4 r = ld_adj4<PF>(r2 + 4 * q);
+            w[4 * q] = r.x;
+            w[4 * q + 1] = r.y;
+            w[4 * q + 2] = r.z;
+            w[4 * q + 3] = r.w;
+        }
     }
-    const uint32_t w[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
     const OffT r0 = RW == 2 ? (OffT)(((uint64_t)w[1] << 32) | w[0]) : (OffT)w[0];
     HB_DCHECK(!act || (int64_t)r0 + deg <= A.arcs, 4);
     // the record's entries: row positions kHeadLen .. kHeadLen + NE - 1

@@ -154,8 +154,12 @@ constexpr int kHeadLen = 3;
 // (words 0-1).  A candidate its head record left open continues here: one
 // sector instead of the row-start sector plus the row's first adjacency
 // sectors, and no dependent row-start load in front of the row.
-__host__ __device__ inline int64_t head2_offset(int64_t n_records) {  // in uint4 units, sector-aligned
-    return (n_records + 2) & ~int64_t(1);
+#ifndef HBFS_H2W
+#define HBFS_H2W 8
+#endif
+constexpr int kH2W = HBFS_H2W;  // words per second-tier record (8 = one sector; 16: experiment)
+__host__ __device__ inline int64_t head2_offset(int64_t n_records) {  // in uint4 units, record-aligned
+    return (n_records + 4) & ~int64_t(3);
 }
 int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const uint32_t *posw,
                 DevBuf &pre, DevBuf &hd, cudaStream_t st, int64_t *n_records = nullptr);

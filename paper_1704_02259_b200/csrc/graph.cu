@@ -222,16 +222,17 @@ __global__ void k_heads(int64_t n, const OffT *rs, const uint32_t *adj, const ui
         h.w = d > 2 ? adj[(uint64_t)s + 2] : HBFS_NIL;
         const int64_t slot = pre[v >> 5] + __popc(posw[v >> 5] & ((1u << (v & 31)) - 1u));
         hd[slot] = h;
-        uint32_t w[8];
+        uint32_t w[kH2W];
         w[0] = (uint32_t)((uint64_t)s & 0xFFFFFFFFu);
         if (RW == 2) w[1] = (uint32_t)((uint64_t)s >> 32);
 #pragma unroll
-        for (int j = RW; j < 8; ++j) {
+        for (int j = RW; j < kH2W; ++j) {
             const uint64_t pos = (uint64_t)kHeadLen + (j - RW);
             w[j] = pos < d ? adj[(uint64_t)s + pos] : HBFS_NIL;
         }
-        hd2[2 * slot] = make_uint4(w[0], w[1], w[2], w[3]);
-        hd2[2 * slot + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int q = 0; q < kH2W / 4; ++q)
+            hd2[(kH2W / 4) * slot + q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
     }
 }
 
@@ -255,7 +256,7 @@ int build_heads(int64_t n, const void *rs, int wide, const uint32_t *adj, const 
     }
     if (n_records) *n_records = (int64_t)total;
     const int64_t off2 = head2_offset((int64_t)total);
-    HB_CHECK(hd.alloc(((size_t)off2 + 2 * ((size_t)total + 1)) * sizeof(uint4)));
+    HB_CHECK(hd.alloc(((size_t)off2 + (kH2W / 4) * ((size_t)total + 1)) * sizeof(uint4)));
     if (n <= 0) return HBFS_OK;
     const int blocks = grid_for(n);
     if (wide)
