@@ -1077,6 +1077,19 @@ __device__ void phase_bu(const Args<OffT> &A, const St &S, const Plane in, const
             }
         }
         __syncwarp();
+        // More than one round of candidates: pull the tile's run of head records
+        // (contiguous, rank-packed) towards L2 now, so that only the first round
+        // waits for DRAM.
+        if (T > 32u * C) {
+            const uint32_t first = __shfl_sync(full, prel, 0);
+            uint32_t npos = __popc(pwl);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) npos += __shfl_xor_sync(full, npos, o);
+            const char *slab = reinterpret_cast<const char *>(A.hd + first);
+            const uint32_t bytes = npos * (uint32_t)sizeof(uint4);
+            for (uint32_t off = lane * 128u; off < bytes; off += 32u * 128u)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(slab + off));
+        }
         uint32_t nopen = 0;  // warp-uniform
         for (uint32_t b = 0; b < T; b += 32 * C) {
             bool act[C];
