@@ -696,9 +696,8 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
                         remote_arc(A, v[k], u[k]);
                         continue;
                     }
-                    // one GPU: the harvest finds the reached vertices by their
-                    // parents (no longer NIL), so an arc costs one reduction, not two
-                    if (PART) atomicOr(&out[v[k] >> 5], b);
+                    // the harvest finds the reached vertices by their parents (no
+                    // longer NIL), so an arc costs one reduction, not two
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
                 }
@@ -1310,7 +1309,7 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
 // graphs).  Reading the parents (268 MB at SCALE 26, streamed) instead of a
 // next-frontier bitmap set by a second reduction per arc: the expansion is
 // bound by the SM's L2 request rate (1 load + 1.5 per reduction, tools/mb).
-// Partitions (PART) keep the bitmap reductions: thread per word.
+// Partitions (PART) harvest their owned words the same way.
 template <typename OffT, bool PART = false>
 __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
                               unsigned long long *red, int32_t depth1) {
@@ -1319,7 +1318,7 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
     const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw;
-    if (!PART) {
+    {
         const unsigned full = 0xffffffffu;
         const int lane = threadIdx.x & 31;
         const int64_t ntiles = (wb - wa + 31) >> 5;
@@ -1366,30 +1365,6 @@ __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned lon
                     for (uint32_t x = f; x; x &= x - 1) {
                         HB_DCHECK(wl * 32 + __ffs(x) - 1 < A.n, 0);
                         A.level[wl * 32 + __ffs(x) - 1] = depth1;
-                    }
-            }
-        }
-    } else {
-        // four words per thread per step: their loads (and the vis words') in flight together
-        for (int64_t w0 = wa + tid; w0 < wb; w0 += 4 * nth) {
-            uint32_t bits[4], vw[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t w = w0 + j * nth;
-                bits[j] = w < wb ? __ldcg(&out[w]) : 0u;  // set by the expansion's reductions
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) vw[j] = bits[j] ? vis[w0 + j * nth] : 0u;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (!bits[j]) continue;
-                const int64_t w = w0 + j * nth;
-                vis[w] = vw[j] | bits[j];
-                acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
-                if (A.direct_levels)
-                    for (uint32_t x = bits[j]; x; x &= x - 1) {
-                        HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
-                        A.level[w * 32 + __ffs(x) - 1] = depth1;
                     }
             }
         }
