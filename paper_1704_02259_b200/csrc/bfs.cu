@@ -63,8 +63,10 @@ constexpr int kCbMaxRanges = 32;
 constexpr int64_t kCbMaxF = 65536;           // frontier entries eligible for blocking
 constexpr int64_t kCbMinArcs = int64_t(1) << 21;
 constexpr int64_t kCbMinN = int64_t(1) << 23;
-// default range count: one per 2^23 targets, 2..16 (measured: S24 best at 2,
-// S26 at 6-8, S28 at 16; more ranges add per-range segment overhead)
+// default range count: one per 2^24 targets, 2..16 (measured: S24 best at 2,
+// S28 at 16; S26 — since the expansion does one reduction per arc — at 4-5:
+// off 937, 2: 998, 3: 1018, 4: 1025, 5: 1025, 6: 1023, 8: 1018, 16: 1001 GTEPS;
+// more ranges add per-range segment overhead)
 constexpr int64_t kCbDefaultRanges = 16;
 // Top-down layers with at least this many frontier arcs expand fire-and-forget
 // and harvest the next frontier from its bitmap (one extra barrier).
@@ -1886,7 +1888,7 @@ static int ws_alloc(hbfs_graph *g) {
     // column blocking for graphs whose parent/level arrays exceed L2
     // (HBFS_CB_MIN_N / HBFS_CB_RANGES: test knobs that force blocking on small graphs)
     const int64_t cb_min_n = env_i64("HBFS_CB_MIN_N", kCbMinN);
-    w->cb_ranges = n >= cb_min_n ? (int)std::min<int64_t>(kCbDefaultRanges, std::max<int64_t>(2, n >> 23)) : 0;
+    w->cb_ranges = n >= cb_min_n ? (int)std::min<int64_t>(kCbDefaultRanges, std::max<int64_t>(2, n >> 24)) : 0;
     if (w->cb_ranges) w->cb_ranges = (int)std::min<int64_t>(31, env_i64("HBFS_CB_RANGES", w->cb_ranges));
     if (!rc && w->cb_ranges) {
         const int64_t P = w->cb_ranges;
@@ -2091,7 +2093,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     if (!rc) rc = T->qo.alloc(2 * (nown + 1) * 8);
     if (!rc) rc = T->qr.alloc(2 * (nown + 1) * 8);
     if (!rc) rc = T->cs.alloc(2 * T->ncs * 4);
-    T->cb_ranges = n >= env_i64("HBFS_CB_MIN_N", kCbMinN) ? (int)std::min<int64_t>(kCbDefaultRanges, std::max<int64_t>(2, n >> 23)) : 0;
+    T->cb_ranges = n >= env_i64("HBFS_CB_MIN_N", kCbMinN) ? (int)std::min<int64_t>(kCbDefaultRanges, std::max<int64_t>(2, n >> 24)) : 0;
     if (!rc && T->cb_ranges) {
         const int64_t P = T->cb_ranges;
         rc = T->cbq.alloc(P * kCbMaxF * 4);
