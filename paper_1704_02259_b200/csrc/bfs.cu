@@ -1823,13 +1823,14 @@ constexpr int kDefaultVariant = 0;
 
 // Measured on B200 (tools/diag.py sweeps): small graphs are latency-bound and
 // prefer one fat CTA per SM with 4 head records in flight per lane (variant 4);
-// SCALE >= 24 prefers two CTAs per SM with 3 per lane (variant 5; S26, 32
-// roots: 2 per lane 1041, 3: 1060, 4: 1046 GTEPS).
+// from 2^22 vertices on two CTAs per SM with 3 per lane win (variant 5; S26, 32
+// roots: 2 per lane 1041, 3: 1060, 4: 1046 GTEPS; variant 4 / 5 at S21 311 / 258,
+// S22 407 / 412, S23 526 / 564, uniform 2^21 213 / 186, uniform 2^22 231 / 253).
 
 static int variant_index(int64_t n) {
     const char *e = getenv("HBFS_KERNEL_VARIANT");
     if (e) return atoi(e);
-    return n >= (int64_t(1) << 24) ? 5 : 4;
+    return n >= (int64_t(1) << 22) ? 5 : 4;
 }
 
 // ------------------------------------------------------------ workspace

@@ -266,11 +266,13 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
                 os.environ[k] = v
 
 
-def test_large_graph_kernel_variant_on_small_graphs(cuda, small_golden, golden_hashes, monkeypatch):
-    """The SCALE>=24 kernel variant (2 CTAs/SM, 4-vector bottom-up probes on
-    tiny-frontier layers) forced on the golden small graphs."""
+@pytest.mark.parametrize("variant", ["5", "3"])
+def test_large_graph_kernel_variant_on_small_graphs(cuda, small_golden, golden_hashes, monkeypatch, variant):
+    """The kernel variants of graphs with n >= 2^22 (2 CTAs/SM, 4-vector bottom-up
+    probes behind small frontiers; 3 — the default there — or 2 head records per
+    lane) forced on the golden small graphs."""
     hb = cuda
-    monkeypatch.setenv("HBFS_KERNEL_VARIANT", "3")
+    monkeypatch.setenv("HBFS_KERNEL_VARIANT", variant)
     for meta in golden_hashes["small"]:
         name = meta["name"]
         p = dict(meta["params"])

@@ -82,8 +82,8 @@ KNOBS = {
     "plain": {},
     # deferred level stamping (depth planes + final pass), normally n >= 2^22
     "defer": {"HBFS_DEFER_LEVELS_MIN_N": "0"},
-    # the large-graph kernel variant (2 searches/lane, scan-tuned bottom-up)
-    "scan_variant": {"HBFS_KERNEL_VARIANT": "3"},
+    # the large-graph kernel variant (3 head records per lane, 2 CTAs/SM)
+    "scan_variant": {"HBFS_KERNEL_VARIANT": "5"},
     # every top-down layer over a bitmap frontier executed by the bottom-up sweep
     # (normally only when few candidates are left); the trace still says top-down
     "bu_exec": {"HBFS_BU_EXEC_RATIO": str(1 << 40)},
