@@ -70,7 +70,10 @@ constexpr int64_t kCbMinN = int64_t(1) << 23;
 constexpr int64_t kCbDefaultRanges = 16;
 // Top-down layers with at least this many frontier arcs expand fire-and-forget
 // and harvest the next frontier from its bitmap (one extra barrier).
-constexpr int64_t kHarvestMinArcs = int64_t(1) << 22;
+constexpr int64_t kHarvestMinArcs = int64_t(1) << 19;
+// ... and from this many on the harvest reads the parents instead of a bitmap
+// set by a second reduction per arc.
+constexpr int64_t kParentHarvestMinArcs = int64_t(1) << 24;
 
 // HB_DCHECK bits (checked builds): 0 parent/level index, 1 bitmap word,
 // 2 queue slot, 3 chunk-start slot, 4 adjacency index, 5 column-blocked
@@ -120,7 +123,7 @@ struct Args {
     Queue<OffT> qb[2];
     Queue<OffT> cbq;  // per-range segment queues: entries r*cb_max_f.., chunk starts r*cb_cs_stride..
     int cb_ranges;
-    int64_t cb_range_len, cb_cs_stride, cb_min_arcs, harvest_min_arcs;
+    int64_t cb_range_len, cb_cs_stride, cb_min_arcs, harvest_min_arcs, parent_harvest_min_arcs;
     Ctl *ctl;
     hbfs_layer_row *rows;
     unsigned long long *phase_ns;  // kPhaseSlots timestamps per trace row (diagnostics)
@@ -632,7 +635,8 @@ template <typename OffT, bool Harvest, int SPAN, bool PART = false>
 __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> &Q, int64_t nf,
                                          uint64_t mf, int64_t c, int64_t nchunks, int32_t depth1,
                                          const Plane in, const Plane out, const Queue<OffT> &NQ,
-                                         Ctr *ctr, TdSmem<OffT> &sm, int sub = 0, int nsub = 1) {
+                                         Ctr *ctr, TdSmem<OffT> &sm, int sub = 0, int nsub = 1,
+                                         bool red_out = false) {
     constexpr int I = kTdItems * SPAN;
     const Plane vis{A.bits};
     const bool any_parent = A.parent_mode == HBFS_PARENT_ANY;
@@ -698,8 +702,11 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
                         remote_arc(A, v[k], u[k]);
                         continue;
                     }
-                    // the harvest finds the reached vertices by their parents (no
-                    // longer NIL), so an arc costs one reduction, not two
+                    // the largest layers: the harvest finds the reached vertices by
+                    // their parents (no longer NIL), an arc costs one reduction;
+                    // mid-size layers also set the next-frontier bit and harvest
+                    // the bitmap (a parent sweep costs more than their reductions)
+                    if (red_out) atomicOr(&out[v[k] >> 5], b);
                     if (any_parent) A.parent[v[k]] = u[k];
                     else atomicMin(&A.parent[v[k]], u[k]);
                 }
@@ -763,7 +770,7 @@ __device__ __forceinline__ void td_chunk(const Args<OffT> &A, const Queue<OffT> 
 // top_down_layer / top_down_chunked (_native.pyx:65-86, :207-239).
 template <typename OffT, bool Harvest, bool PART = false>
 __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
-                         const Plane spare, Ctr *ctr, TdSmem<OffT> &sm) {
+                         const Plane spare, Ctr *ctr, TdSmem<OffT> &sm, bool red_out = false) {
     const Queue<OffT> &Q = A.qb[S.layer & 1];
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
     if (!Harvest) td_prologue<OffT, PART>(A, S, spare);  // harvest layers run it before a barrier
@@ -778,7 +785,7 @@ __device__ void phase_td(const Args<OffT> &A, const St &S, const Plane in, const
         while (nsub < kTdMaxSub && nitems * nsub * 4 <= (int64_t)gridDim.x) nsub *= 2;
     for (int64_t g = blockIdx.x; g < nitems * nsub; g = block_grab(work, &sm.item))
         td_chunk<OffT, Harvest, SPAN, PART>(A, Q, nf, mf, (g / nsub) * SPAN, nchunks, (int32_t)S.layer + 1,
-                                            in, out, NQ, ctr, sm, (int)(g % nsub), nsub);
+                                            in, out, NQ, ctr, sm, (int)(g % nsub), nsub, red_out);
 }
 
 template <typename OffT>
@@ -847,7 +854,7 @@ __device__ void phase_cb_build(const Args<OffT> &A, const St &S, const Plane spa
 // target range at a time.
 template <typename OffT, bool Harvest, bool PART = false>
 __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, const Plane out,
-                             Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre) {
+                             Ctr *ctr, int bank, TdSmem<OffT> &sm, int64_t *s_pre, bool red_out = false) {
     const int P = A.cb_ranges;
     const Queue<OffT> &NQ = A.qb[(S.layer + 1) & 1];
     constexpr int SPAN = Harvest ? 2 : 1;
@@ -873,7 +880,7 @@ __device__ void phase_cb_run(const Args<OffT> &A, const St &S, const Plane in, c
         const Queue<OffT> R = cb_queue(A, r, kCbMaxF);
         const int64_t nch_r = (int64_t)((mf_r + kTdChunk - 1) / kTdChunk);
         td_chunk<OffT, Harvest, SPAN, PART>(A, R, nf_r, mf_r, (g - s_pre[r]) * SPAN, nch_r,
-                                            (int32_t)S.layer + 1, in, out, NQ, ctr, sm);
+                                            (int32_t)S.layer + 1, in, out, NQ, ctr, sm, 0, 1, red_out);
     }
 }
 
@@ -1314,13 +1321,38 @@ __device__ void phase_convert(const Args<OffT> &A, const Queue<OffT> &Q, const P
 // Partitions (PART) harvest their owned words the same way.
 template <typename OffT, bool PART = false>
 __device__ void phase_harvest(const Args<OffT> &A, const Plane out, unsigned long long *counter,
-                              unsigned long long *red, int32_t depth1) {
+                              unsigned long long *red, int32_t depth1, bool by_bitmap) {
     const Plane vis{A.bits};
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long acc = 0;  // packed count<<35 | degree sum
     const int64_t wa = PART ? A.part_w0 : 0, wb = PART ? A.part_wend : A.nw;
-    {
+    if (by_bitmap) {
+        // mid-size layers: the expansion set the next-frontier bits; thread per
+        // word, four words per step with their loads in flight together
+        for (int64_t w0 = wa + tid; w0 < wb; w0 += 4 * nth) {
+            uint32_t bits[4], vw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t w = w0 + j * nth;
+                bits[j] = w < wb ? __ldcg(&out[w]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) vw[j] = bits[j] ? vis[w0 + j * nth] : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!bits[j]) continue;
+                const int64_t w = w0 + j * nth;
+                vis[w] = vw[j] | bits[j];
+                acc += ((unsigned long long)__popc(bits[j]) << kPackShift) + word_degsum(A, w, bits[j]);
+                if (A.direct_levels)
+                    for (uint32_t x = bits[j]; x; x &= x - 1) {
+                        HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
+                        A.level[w * 32 + __ffs(x) - 1] = depth1;
+                    }
+            }
+        }
+    } else {
         const unsigned full = 0xffffffffu;
         const int lane = threadIdx.x & 31;
         const int64_t ntiles = (wb - wa + 31) >> 5;
@@ -1621,19 +1653,25 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             if (!PART) A.ctl->conv = 0;  // PART: the host resets it (other CTAs read it above)
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
+        // Top-down regimes by frontier arcs: claim path (builds the next queue),
+        // from harvest_min_arcs fire-and-forget expansion + harvest — of the
+        // next-frontier bitmap set by a second reduction per arc, or, from
+        // parent_harvest_min_arcs, of the parents (one reduction per arc, but a
+        // sweep over every unvisited vertex's parent).
         const bool harvest = xdir == HBFS_TOP_DOWN && SQ.e_f >= A.harvest_min_arcs;
+        const bool red_out = harvest && SQ.e_f < A.parent_harvest_min_arcs;
         if (cb) {
             phase_cb_build<OffT, PART>(A, SQ, spare, (int)(L & 1));
             grid.sync();
             STAMP(2);
-            if (harvest) phase_cb_run<OffT, true, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
+            if (harvest) phase_cb_run<OffT, true, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre, red_out);
             else phase_cb_run<OffT, false, PART>(A, SQ, in, out, ctr, (int)(L & 1), sm, s_pre);
         } else if (xdir == HBFS_TOP_DOWN) {
             if (harvest) {
                 td_prologue<OffT, PART>(A, SQ, spare);
                 grid.sync();  // vis now holds the frontier: the expansion tests vis alone
                 STAMP(2);
-                phase_td<OffT, true, PART>(A, SQ, in, out, spare, ctr, sm);
+                phase_td<OffT, true, PART>(A, SQ, in, out, spare, ctr, sm, red_out);
             } else {
                 phase_td<OffT, false, PART>(A, SQ, in, out, spare, ctr, sm);
             }
@@ -1641,7 +1679,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         if (harvest) {
             grid.sync();
             STAMP(3);
-            phase_harvest<OffT, PART>(A, out, &ctr->packed, red, (int32_t)L + 1);
+            phase_harvest<OffT, PART>(A, out, &ctr->packed, red, (int32_t)L + 1, red_out);
         }
         if (xdir == HBFS_BOTTOM_UP) {
             uint32_t *sf = s_found + (threadIdx.x & ~31);
@@ -1964,6 +2002,7 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.cb_cs_stride = w->ncs;
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
     A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
+    A.parent_harvest_min_arcs = env_i64("HBFS_PARENT_HARVEST_MIN_ARCS", kParentHarvestMinArcs);
     // level arrays that fit L2 take scattered stores cheaply; larger graphs
     // stamp levels once from the depth planes (HBFS_DEFER_LEVELS_MIN_N: test knob)
     A.direct_levels = g->n < env_i64("HBFS_DEFER_LEVELS_MIN_N", int64_t(1) << 22);
@@ -2153,6 +2192,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.cb_cs_stride = T->ncs;
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
     A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
+    A.parent_harvest_min_arcs = env_i64("HBFS_PARENT_HARVEST_MIN_ARCS", kParentHarvestMinArcs);
     A.direct_levels = 1;
     A.ctl = T->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(T->ctl.as<char>() + sizeof(Ctl));

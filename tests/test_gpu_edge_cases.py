@@ -221,8 +221,9 @@ def test_reference_csr_import(cuda, oracle):
     assert np.array_equal(tree.parent, par) and len(trace) == len(rows)
 
 
-@pytest.mark.parametrize("cb,harvest", [(True, False), (True, True), (False, True)])
-def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, cb, harvest):
+@pytest.mark.parametrize("cb,harvest,by_parent", [(True, False, False), (True, True, False), (False, True, False),
+                                                  (True, True, True), (False, True, True)])
+def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, cb, harvest, by_parent):
     """Force the large-layer top-down strategies on the golden small graphs:
     column blocking (every frontier row split into target ranges, normally
     SCALE >= 23 hub layers) and/or the harvest path (fire-and-forget expansion +
@@ -231,11 +232,13 @@ def test_top_down_strategies_forced(cuda, oracle, small_golden, golden_hashes, c
 
     hb = cuda
     keys = ("HBFS_CB_MIN_N", "HBFS_CB_MIN_ARCS", "HBFS_CB_RANGES", "HBFS_HARVEST_MIN_ARCS",
-            "HBFS_DEFER_LEVELS_MIN_N")
+            "HBFS_DEFER_LEVELS_MIN_N", "HBFS_PARENT_HARVEST_MIN_ARCS")
     old = {k: os.environ.get(k) for k in keys}
     os.environ.update(HBFS_CB_MIN_N="0" if cb else str(1 << 40), HBFS_CB_MIN_ARCS="0",
                       HBFS_CB_RANGES="7", HBFS_HARVEST_MIN_ARCS="0" if harvest else str(1 << 40),
-                      HBFS_DEFER_LEVELS_MIN_N="0" if harvest else str(1 << 40))
+                      HBFS_DEFER_LEVELS_MIN_N="0" if harvest else str(1 << 40),
+                      # harvest of the parents (normally >= 2^24 arcs) or of the bitmap
+                      HBFS_PARENT_HARVEST_MIN_ARCS="0" if by_parent else str(1 << 40))
     try:
         for meta in golden_hashes["small"]:
             name = meta["name"]
