@@ -135,6 +135,9 @@ struct Args {
     int64_t part_w0, part_wend;  // partition (PART): owned word range
     int64_t part_lo, part_nown;  // partition (PART): owned vertex range
     uint32_t *cand, *touch;      // partition top-down: remote targets' min parent / touched bits
+    int64_t pst[6];              // partition: the global controller state of this layer (layer, v_f, e_f, eu_v, eu_e, prev_vf)
+    int32_t pdir;                // partition: the previous layer's direction
+    unsigned long long *lay_out; // partition: this rank's layer totals {found, degree sum, gathers, fallbacks} (may be null)
     uint32_t root;
 };
 
@@ -1591,7 +1594,16 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         S.prev_vf = 0;
         S.dir = HBFS_TOP_DOWN;
         S.kind = 0;
-    } else {  // resumed, or (PART) the global state written by the host
+    } else if (PART) {  // the global state, from the host loop
+        S.layer = A.pst[0];
+        S.v_f = A.pst[1];
+        S.e_f = A.pst[2];
+        S.eu_v = A.pst[3];
+        S.eu_e = A.pst[4];
+        S.prev_vf = A.pst[5];
+        S.dir = A.pdir;
+        S.kind = 1;
+    } else {  // resumed
         const Ctl *c = A.ctl;
         S.layer = __ldcg(&c->layer);
         S.v_f = __ldcg(&c->v_f);
@@ -1650,7 +1662,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         if (leader) {
             A.ctl->ctr[(L + 1) % 3] = Ctr{0, 0, 0, 0};
             A.ctl->work[(L + 1) % 3] = 0;
-            if (!PART) A.ctl->conv = 0;  // PART: the host resets it (other CTAs read it above)
+            if (!PART) A.ctl->conv = 0;  // PART: reset at the end of the layer (other CTAs read it above)
             for (int r = 0; r < kCbMaxRanges; ++r) A.ctl->cbctr[(L + 1) & 1][r] = 0;
         }
         // Top-down regimes by frontier arcs: claim path (builds the next queue),
@@ -1732,6 +1744,15 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
             r.elapsed = (double)(now - t_start) * 1e-9;
             A.rows[rows] = r;
             t_start = now;
+            if (PART) {
+                A.ctl->conv = 0;  // every CTA read it barriers ago; free for the next launch
+                if (A.lay_out) {  // this rank's totals, for the host loop's single read-back
+                    A.lay_out[0] = (unsigned long long)nvf;
+                    A.lay_out[1] = (unsigned long long)nef;
+                    A.lay_out[2] = __ldcg(&ctr->gathers);
+                    A.lay_out[3] = __ldcg(&ctr->fallbacks);
+                }
+            }
         }
         S.prev_vf = S.v_f;
         S.v_f = nvf;
@@ -2107,10 +2128,6 @@ struct PartTrav {
     size_t smem = 0;
     DevBuf bits, q, qo, qr, cs, cbq, cbqo, cbqr, cbcs, ctl, phases;
     Args<uint64_t> A;
-    void *h_state = nullptr;  // pinned staging of the controller state written before each launch
-    ~PartTrav() {
-        if (h_state) cudaFreeHost(h_state);
-    }
 };
 
 static const void *part_kernel() { return (const void *)bfs_kernel<uint64_t, 2, 2, true, true>; }
@@ -2143,7 +2160,6 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     }
     if (!rc) rc = T->ctl.alloc(ctl_bytes());
     if (!rc) rc = T->phases.alloc((kRowsCap + 1) * kPhaseSlots * 8);
-    if (!rc && cudaMallocHost(&T->h_state, 256) != cudaSuccess) rc = set_error(HBFS_ECUDA, "cudaMallocHost failed");
     if (!rc) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
@@ -2235,7 +2251,7 @@ int part_trav_add_counters(void *h, int64_t layer, const unsigned long long *app
 }
 
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, int64_t n_pos_global, cudaStream_t st) {
+                    const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out, cudaStream_t st) {
     PartTrav *T = static_cast<PartTrav *>(h);
     Args<uint64_t> A = T->A;
     A.H.heuristic = p->heuristic;
@@ -2251,19 +2267,10 @@ int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, u
     A.do_init = do_init;
     A.n_pos = n_pos_global;
     A.bu_exec_ratio = bu_exec_ratio();
-    struct {
-        int64_t layer, v_f, e_f, eu_v, eu_e, prev_vf;
-        int32_t dir, kind, done;
-        uint32_t lv_done;
-        int64_t rows;
-        unsigned long long conv;
-    } hs = {state[0], state[1], state[2], state[3], state[4], state[5], dir, 1, 0, 0u, 0, 0ull};
-    static_assert(offsetof(Ctl, conv) + sizeof(unsigned long long) == sizeof(hs), "Ctl head layout");
-    static_assert(sizeof(hs) <= 256, "state staging");
-    // pinned staging: the caller synchronises the stream once per layer, so the
-    // previous layer's copy has been consumed
-    memcpy(T->h_state, &hs, sizeof(hs));
-    HB_CUDA(cudaMemcpyAsync(A.ctl, T->h_state, sizeof(hs), cudaMemcpyHostToDevice, st));
+    // the controller state travels in the kernel arguments: no copy per layer
+    for (int i = 0; i < 6; ++i) A.pst[i] = state[i];
+    A.pdir = dir;
+    A.lay_out = lay_out;
     void *kargs[] = {&A};
     HB_CUDA(cudaLaunchCooperativeKernel(part_kernel(), dim3(T->grid), dim3(kBlock), kargs, T->smem, st));
     return HBFS_OK;

@@ -1044,11 +1044,15 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
         // partition with more than one rank needs one more, for the record
         // counts NCCL takes from the host.
         unsigned long long *lay = P0->lay.as<unsigned long long>();
-        HB_CUDA(cudaMemsetAsync(lay, 0, 32, st));
-        for (int i = 0; i < nparts; ++i)  // asynchronous
-            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, n_pos, st));
         // records only after a real top-down expansion with remote targets
         const bool exchange = d == HBFS_TOP_DOWN && world > 1 && !bu_executes(d, 1, eu_v, e_f, n, n_pos, ratio);
+        // one part in this process and no records to add: the kernel itself
+        // leaves the layer totals in `lay`
+        const bool direct = nparts == 1 && !exchange;
+        if (!direct) HB_CUDA(cudaMemsetAsync(lay, 0, 32, st));
+        for (int i = 0; i < nparts; ++i)  // asynchronous
+            HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, n_pos,
+                                     direct ? lay : nullptr, st));
         if (exchange) {
             for (int i = 0; i < nparts; ++i)
                 HB_CHECK(td_owner_counts(Ps[i], world, wper, Ps[i]->counts_dev.as<int64_t>(), st));
@@ -1131,9 +1135,10 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
                                                                P->acnt.as<unsigned long long>());
             }
         }
-        for (int i = 0; i < nparts; ++i)
-            HB_CHECK(part_trav_add_counters(Ps[i]->trav, layer, exchange ? Ps[i]->acnt.as<unsigned long long>() : nullptr,
-                                            lay, st));
+        if (!direct)
+            for (int i = 0; i < nparts; ++i)
+                HB_CHECK(part_trav_add_counters(Ps[i]->trav, layer,
+                                                exchange ? Ps[i]->acnt.as<unsigned long long>() : nullptr, lay, st));
         // next frontier: every rank's owned words of plane layer+1 to everyone
         // (the next launch ORs the all-gathered plane into the visited bitmap)
         if (M && world > 1) {
