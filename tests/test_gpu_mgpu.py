@@ -176,3 +176,30 @@ def test_exchange_stats_and_pinned_outputs(cuda):
     # top-down layers over few remaining candidates run as local bottom-up sweeps: no records
     assert st[0]["layers"] == len(res.trace) and 0 < st[0]["record_exchanges"] <= len(res.trace)
     assert st[0]["records_sent"] == st[1]["records_received"] > 0
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_persistent_partition_deep_traversal(cuda, oracle, world):
+    """More layers than the depth-plane ring holds (32): a 150-vertex path with
+    a few chords, through the C++ loop over the persistent partition kernel."""
+    hb = cuda
+    from paper_1704_02259_b200.mgpu import CudaRankOps, LocalPersistBfs
+
+    n = 160
+    u = np.arange(0, 149, dtype=np.uint32)
+    v = u + 1
+    u = np.concatenate([u, np.array([3, 40, 90], dtype=np.uint32)])
+    v = np.concatenate([v, np.array([7, 44, 97], dtype=np.uint32)])
+    host = oracle.csr_build(u, v, n)
+    ranks = [CudaRankOps.from_csr(host.row_starts, host.adjacency, host.in_edges_total, world, r)
+             for r in range(world)]
+    db = LocalPersistBfs(ranks)
+    for s in (0, 75, 149):
+        res = db.bfs(s, use_simd=True)
+        outs = db.outputs()
+        par = np.concatenate([o[0] for o in outs])
+        lev = np.concatenate([o[1] for o in outs])
+        want_p, want_l, rows = oracle.hybrid_bfs(host, s, use_simd=True)
+        assert np.array_equal(lev, want_l), (world, s)
+        assert np.array_equal(par, want_p), (world, s)
+        assert len(res.trace) == len(rows) and len(rows) > 40
