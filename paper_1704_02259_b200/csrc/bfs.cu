@@ -11,17 +11,23 @@
 //   rs     OffT[n+1]    row starts (uint32 when arcs < 2^32, else uint64)
 //   adj    u32[arcs]    sorted rows (csr.py:61-64)
 //   posw   u32[W]       deg>0 bitmap (engine.py:29-57 `posw`)
+//   hd     uint4[R]     head records {degree, row[0..2]}, rank-packed over the R
+//                        vertices with degree > 0; behind them (same slots) the
+//                        32-byte second-tier records {row start, row[3..9]}
+//   pre    u32[W+1]     head records before bitmap word w
 //   parent u32[n], level i32[n]
-//   bits   u32[5W]      vis | B0 | B1 | B2 | B3 — LSB-first bitmaps (frontier.py:3-6)
+//   bits   u32[33W]     vis | a ring of kPlanes depth planes — LSB-first bitmaps
+//                        (frontier.py:3-6); plane 1 + d % kPlanes holds depth d
 //   q/qo/qr             frontier queue: vertex, exclusive degree prefix (arc
 //                        offset), row start — double-buffered
 //   cs     u32[2*NC]    chunk starts: queue index holding arc c*kTdChunk
 //
 // Invariants at the start of layer L (frontier = depth L):
-//   in  = B[L%4] = frontier bitmap; out = B[(L+1)%4] is all-zero;
-//   spare = B[(L+2)%4] is cleared during L (B[(L+3)%4] is the previous frontier)
+//   in  = plane(L) = frontier bitmap; out = plane(L+1) is all-zero;
+//   spare = plane(L+2) is cleared during L (its levels stamped first if the ring wrapped)
 //   vis | in = every vertex discovered so far (vis may lag by the frontier)
-//   queue buffer L%2 valid iff the frontier was produced top-down (kind 0)
+//   queue buffer L%2 valid iff the frontier was produced by the top-down claim
+//   path (kind 0); harvest and bottom-up layers leave only the bitmap (kind 1)
 // Parents follow the reference's rule: the minimum-id neighbour one
 // level up.  Bottom-up layers get it directly (first hit in the sorted row);
 // top-down layers take the atomicMin over every arc into a vertex unvisited
