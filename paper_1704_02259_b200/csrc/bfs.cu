@@ -141,6 +141,8 @@ struct Args {
     int64_t part_w0, part_wend;  // partition (PART): owned word range
     int64_t part_lo, part_nown;  // partition (PART): owned vertex range
     uint32_t *cand, *touch;      // partition top-down: remote targets' min parent / touched bits
+    int64_t lv_w0, lv_wend;      // bitmap words whose levels this process stamps (all, or a partition's owned words)
+    int64_t lv_layers;           // level pass: layer count from the host (partitions), < 0: from the controller state
     int64_t pst[6];              // partition: the global controller state of this layer (layer, v_f, e_f, eu_v, eu_e, prev_vf)
     int32_t pdir;                // partition: the previous layer's direction
     unsigned long long *lay_out; // partition: this rank's layer totals {found, degree sum, gathers, fallbacks} (may be null)
@@ -217,7 +219,7 @@ __device__ __forceinline__ void clear_spare_word(const A_t &A, int64_t L, int64_
     }
     uint32_t x = *p;
     if (!x) return;
-    {
+    if (w >= A.lv_w0 && w < A.lv_wend) {  // (a partition stamps its owned vertices only)
         const int32_t d = (int32_t)(L + 2 - kPlanes);
         while (x) {
             HB_DCHECK(w * 32 + __ffs(x) - 1 < A.n, 0);
@@ -1454,13 +1456,14 @@ __device__ __forceinline__ int32_t sext_byte(uint32_t x) {
 template <typename OffT>
 __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
     const Ctl *c = A.ctl;
-    if (!__ldcg(&c->done)) return;
+    if (A.lv_layers < 0 && !__ldcg(&c->done)) return;
     unsigned long long *kstamp = A.phase_ns + kRowsCap * kPhaseSlots;
     if (blockIdx.x == 0 && threadIdx.x == 0) kstamp[3] = globaltimer();
-    const int64_t nL = __ldcg(&c->layer);
+    const int64_t nL = A.lv_layers >= 0 ? A.lv_layers : __ldcg(&c->layer);
+    const int64_t lw0 = A.lv_w0, lwend = A.lv_wend;  // words stamped here
     const int lane = threadIdx.x & 31;
     const int64_t d0 = nL + 2 - kPlanes > 0 ? nL + 2 - kPlanes : 0;
-    const int64_t ntiles = (A.nw + 31) / 32;
+    const int64_t ntiles = (lwend - lw0 + 31) / 32;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const bool aligned = (reinterpret_cast<uintptr_t>(A.level) & 15) == 0;
@@ -1476,8 +1479,8 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
     uint32_t(*st)[kLvBatch + 1][32] = stage[threadIdx.x >> 5];
     const int nrow = (int)(nL - d0) + 1;  // planes d0..nL-1, then the visited row
     auto load_tile = [&](int64_t t, int s) {
-        const int64_t w = t * 32 + lane;
-        const unsigned sz = t < ntiles && w < A.nw ? 4u : 0u;  // zero-fill past the end
+        const int64_t w = lw0 + t * 32 + lane;
+        const unsigned sz = t < ntiles && w < lwend ? 4u : 0u;  // zero-fill past the end
         const int64_t wc = sz ? w : 0;
         for (int j = 0; j < nrow; ++j) {
             const uint32_t *src = j + 1 < nrow ? depth_plane(A, d0 + j).p + wc : A.bits + wc;
@@ -1489,7 +1492,7 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
     int s = 0;
     if (one_batch) load_tile(warp, 0);
     for (int64_t t = warp; t < ntiles; t += nwarps, s ^= 1) {
-        const int64_t w = t * 32 + lane;
+        const int64_t w = lw0 + t * 32 + lane;
         uint32_t R = 0, D[5] = {0, 0, 0, 0, 0}, vw;
         if (one_batch) {
             load_tile(t + nwarps, s ^ 1);  // in flight while this tile is stored
@@ -1504,12 +1507,12 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
             vw = st[s][nrow - 1][lane];
             __syncwarp();  // stage s is refilled next iteration
         } else {  // deep traversals: all held planes, batch by batch
-            vw = w < A.nw ? __ldcs(A.bits + w) : 0u;
+            vw = w < lwend ? __ldcs(A.bits + w) : 0u;
             for (int64_t g0 = d0; g0 < nL; g0 += kLvBatch) {
                 uint32_t p[kLvBatch];
 #pragma unroll
                 for (int j = 0; j < kLvBatch; ++j)
-                    p[j] = w < A.nw && g0 + j < nL ? __ldcs(depth_plane(A, g0 + j).p + w) : 0u;
+                    p[j] = w < lwend && g0 + j < nL ? __ldcs(depth_plane(A, g0 + j).p + w) : 0u;
 #pragma unroll
                 for (int j = 0; j < kLvBatch; ++j) {
                     const uint32_t rel = (uint32_t)(g0 + j - d0);
@@ -1519,7 +1522,8 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
                 }
             }
         }
-        const bool fast = d0 == 0 && (t * 32 + 32) * 32 <= A.n && aligned;  // warp-uniform
+        const bool fast = d0 == 0 && lw0 + t * 32 + 32 <= lwend && (lw0 + t * 32 + 32) * 32 <= A.n &&
+                          aligned;  // warp-uniform
         if (fast) {
             // round r: the warp writes words 4r..4r+3 of the tile (512
             // contiguous bytes, four full lines); lane l takes levels
@@ -1540,11 +1544,11 @@ __global__ void __launch_bounds__(kLvBlock) levels_kernel(Args<OffT> A) {
                 }
                 const uint32_t hit = (((__shfl_sync(0xffffffffu, R, src) >> b0) & 0xFu) * 0x00204081u) & 0x01010101u;
                 v |= (hit ^ 0x01010101u) * 0xFFu;
-                HB_DCHECK((t * 32 + src) * 32 + 32 <= A.n, 7);
-                int4 *gdst = reinterpret_cast<int4 *>(A.level + (t * 32 + src) * 32);
+                HB_DCHECK((lw0 + t * 32 + src) * 32 + 32 <= A.n, 7);
+                int4 *gdst = reinterpret_cast<int4 *>(A.level + (lw0 + t * 32 + src) * 32);
                 __stcs(gdst + (lane & 7), make_int4(sext_byte<0>(v), sext_byte<1>(v), sext_byte<2>(v), sext_byte<3>(v)));
             }
-        } else if (w < A.nw) {
+        } else if (w < lwend) {
             int32_t *dst = A.level + w * 32;
             HB_DCHECK(w < A.nw, 7);
             for (int b = 0; b < 32; ++b) {
@@ -2013,6 +2017,9 @@ static int run_bfs(hbfs_graph *g, uint32_t root, const hbfs_params *p, uint32_t 
     A.posw = g->posw.as<uint32_t>();
     A.hd = g->hd.as<uint4>();
     A.hd2 = g->hd.as<uint4>() + head2_offset(g->n_pos);
+    A.lv_w0 = 0;
+    A.lv_wend = g->nw;
+    A.lv_layers = -1;
     A.pre = g->pre.as<uint32_t>();
     A.n_pos = g->n_pos;
     A.bu_exec_ratio = bu_exec_ratio();
@@ -2215,7 +2222,12 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
     A.cb_min_arcs = env_i64("HBFS_CB_MIN_ARCS", kCbMinArcs);
     A.harvest_min_arcs = env_i64("HBFS_HARVEST_MIN_ARCS", kHarvestMinArcs);
     A.parent_harvest_min_arcs = env_i64("HBFS_PARENT_HARVEST_MIN_ARCS", kParentHarvestMinArcs);
-    A.direct_levels = 1;
+    // as on one GPU: large graphs record depths in the plane ring and stamp the
+    // owned levels once at the end (part_trav_levels)
+    A.direct_levels = n < env_i64("HBFS_DEFER_LEVELS_MIN_N", int64_t(1) << 22);
+    A.lv_w0 = lo >> 5;
+    A.lv_wend = (lo >> 5) + (nown + 31) / 32;
+    A.lv_layers = -1;
     A.ctl = T->ctl.as<Ctl>();
     A.rows = reinterpret_cast<hbfs_layer_row *>(T->ctl.as<char>() + sizeof(Ctl));
     A.rows_cap = 1;
@@ -2235,6 +2247,28 @@ void part_trav_free(void *h) { delete static_cast<PartTrav *>(h); }
 uint32_t *part_trav_plane(void *h, int64_t depth) {
     PartTrav *T = static_cast<PartTrav *>(h);
     return depth < 0 ? T->bits.as<uint32_t>() : T->bits.as<uint32_t>() + T->nw * (1 + depth % kPlanes);
+}
+
+// After the last layer: stamp the owned levels from the depth planes (no-op
+// when levels were stamped at discovery).  nL: layers of the traversal.
+int part_trav_levels(void *h, int64_t nL, cudaStream_t st) {
+    PartTrav *T = static_cast<PartTrav *>(h);
+    if (T->A.direct_levels) return HBFS_OK;
+    Args<uint64_t> A = T->A;
+    A.lv_layers = nL;
+    static int lv_grid = 0;
+    if (!lv_grid) {
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, levels_kernel<uint64_t>, kLvBlock, 0);
+        lv_grid = std::max(1, per_sm) * sms;
+    }
+    const int64_t tiles = (A.lv_wend - A.lv_w0 + 31) / 32, per = kLvBlock / 32;
+    const int64_t blocks = std::min<int64_t>((tiles + per - 1) / per, (int64_t)lv_grid);
+    levels_kernel<uint64_t><<<(unsigned)std::max<int64_t>(1, blocks), kLvBlock, 0, st>>>(A);
+    HB_CUDA(cudaGetLastError());
+    return HBFS_OK;
 }
 
 // One layer, asynchronous: the global controller state in; this rank's

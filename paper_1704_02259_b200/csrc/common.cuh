@@ -195,6 +195,7 @@ void *part_trav_create(int64_t n, int64_t lo, int64_t nown, int64_t arcs_local, 
                        int32_t *level_local, uint32_t *cand, uint32_t *touch, int *rc_out, int64_t nw_pad);
 void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
+int part_trav_levels(void *h, int64_t n_layers, cudaStream_t st);  // final level stamp of the owned vertices
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
                     const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out,
                     cudaStream_t st);  // asynchronous; lay_out (device, may be null): the rank's layer totals

@@ -1180,6 +1180,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
         cur = d;
         ++layer;
     }
+    for (int i = 0; i < nparts; ++i) HB_CHECK(part_trav_levels(Ps[i]->trav, layer, st));
     HB_CUDA(cudaEventRecord(ev1, st));
     HB_CUDA(cudaEventSynchronize(ev1));
     if (device_ms) HB_CUDA(cudaEventElapsedTime(device_ms, ev0, ev1));

@@ -92,13 +92,15 @@ def test_nccl_loop_single_rank(cuda, small_golden, name):
 
 @pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("name", ["k8", "k10", "u12"])
-def test_persistent_partition_kernel(cuda, small_golden, world, name):
+def test_persistent_partition_kernel(cuda, small_golden, world, name, monkeypatch):
     """P ranks of the persistent partition kernel (one launch per layer, the
     C++ loop with device-copy exchanges) on one GPU: levels, min-id parents and
     the trace equal the reference's."""
     hb = cuda
     from paper_1704_02259_b200.mgpu import CudaRankOps, LocalPersistBfs
 
+    if world == 2:  # also the large graphs' deferred level stamping (depth planes + final pass per rank)
+        monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", "0")
     rs, adj = small_golden[f"{name}/rs"], small_golden[f"{name}/adj"]
     ranks = [CudaRankOps.from_csr(rs, adj, len(adj) // 2, world, r) for r in range(world)]
     lb = LocalPersistBfs(ranks)
@@ -178,12 +180,17 @@ def test_exchange_stats_and_pinned_outputs(cuda):
     assert st[0]["records_sent"] == st[1]["records_received"] > 0
 
 
+@pytest.mark.parametrize("defer", ["0", str(1 << 40)])
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_persistent_partition_deep_traversal(cuda, oracle, world):
+def test_persistent_partition_deep_traversal(cuda, oracle, world, defer, monkeypatch):
     """More layers than the depth-plane ring holds (32): a 150-vertex path with
-    a few chords, through the C++ loop over the persistent partition kernel."""
+    a few chords, through the C++ loop over the persistent partition kernel —
+    with levels stamped at discovery and with the deferred stamping of large
+    graphs (ring flush of the owned words + final level pass per rank)."""
     hb = cuda
     from paper_1704_02259_b200.mgpu import CudaRankOps, LocalPersistBfs
+
+    monkeypatch.setenv("HBFS_DEFER_LEVELS_MIN_N", defer)
 
     n = 160
     u = np.arange(0, 149, dtype=np.uint32)
