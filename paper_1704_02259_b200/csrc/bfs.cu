@@ -145,6 +145,7 @@ struct Args {
     int64_t lv_layers;           // level pass: layer count from the host (partitions), < 0: from the controller state
     int64_t pst[6];              // partition: the global controller state of this layer (layer, v_f, e_f, eu_v, eu_e, prev_vf)
     int32_t pdir;                // partition: the previous layer's direction
+    int32_t part_single;         // partition: the only rank (no exchange: queues stay valid across layers)
     unsigned long long *lay_out; // partition: this rank's layer totals {found, degree sum, gathers, fallbacks} (may be null)
     uint32_t root;
 };
@@ -1612,7 +1613,9 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         S.eu_e = A.pst[4];
         S.prev_vf = A.pst[5];
         S.dir = A.pdir;
-        S.kind = 1;
+        // the frontier arrives as an all-gathered bitmap; a single-rank partition
+        // keeps the queue its own claim path built (as on one GPU)
+        S.kind = A.part_single && !A.do_init ? __ldcg(&A.ctl->kind) : 1;
     } else {  // resumed
         const Ctl *c = A.ctl;
         S.layer = __ldcg(&c->layer);
@@ -1654,7 +1657,7 @@ __global__ void __launch_bounds__(kBlock, MINB) bfs_kernel(Args<OffT> A) {
         // the rank, and the host loop takes the same decision — bu_executes — to
         // skip the record exchange)
         if (bu_executes(xdir, S.kind, S.eu_v, S.e_f, A.n, A.n_pos, A.bu_exec_ratio)) xdir = HBFS_BOTTOM_UP;
-        if (xdir == HBFS_TOP_DOWN && (PART || S.kind == 1)) {
+        if (xdir == HBFS_TOP_DOWN && S.kind == 1) {
             phase_convert<OffT, PART>(A, A.qb[L & 1], in, &A.ctl->conv, false, sm.enq);
             grid.sync();
             STAMP(1);
@@ -2291,7 +2294,8 @@ int part_trav_add_counters(void *h, int64_t layer, const unsigned long long *app
 }
 
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out, cudaStream_t st) {
+                    const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out, int single,
+                    cudaStream_t st) {
     PartTrav *T = static_cast<PartTrav *>(h);
     Args<uint64_t> A = T->A;
     A.H.heuristic = p->heuristic;
@@ -2310,6 +2314,7 @@ int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, u
     // the controller state travels in the kernel arguments: no copy per layer
     for (int i = 0; i < 6; ++i) A.pst[i] = state[i];
     A.pdir = dir;
+    A.part_single = single;
     A.lay_out = lay_out;
     void *kargs[] = {&A};
     HB_CUDA(cudaLaunchCooperativeKernel(part_kernel(), dim3(T->grid), dim3(kBlock), kargs, T->smem, st));

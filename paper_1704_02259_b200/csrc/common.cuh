@@ -197,7 +197,7 @@ void part_trav_free(void *h);
 uint32_t *part_trav_plane(void *h, int64_t depth);  // depth < 0: the visited bitmap
 int part_trav_levels(void *h, int64_t n_layers, cudaStream_t st);  // final level stamp of the owned vertices
 int part_trav_layer(void *h, const int64_t state[6], int32_t dir, int do_init, uint32_t root,
-                    const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out,
+                    const hbfs_params *p, int64_t n_pos_global, unsigned long long *lay_out, int single,
                     cudaStream_t st);  // asynchronous; lay_out (device, may be null): the rank's layer totals
 // tot[0..3] += this rank's counters of `layer` (+ applied[0..1], the records it applied), on the stream
 int part_trav_add_counters(void *h, int64_t layer, const unsigned long long *applied, unsigned long long *tot,

@@ -1052,7 +1052,7 @@ static int persist_loop(hbfs_part **Ps, int nparts, hbfs_mg *M, int world, int64
         if (!direct) HB_CUDA(cudaMemsetAsync(lay, 0, 32, st));
         for (int i = 0; i < nparts; ++i)  // asynchronous
             HB_CHECK(part_trav_layer(Ps[i]->trav, state, cur, layer == 0, (uint32_t)root, p, n_pos,
-                                     direct ? lay : nullptr, st));
+                                     direct ? lay : nullptr, world == 1, st));
         if (exchange) {
             for (int i = 0; i < nparts; ++i)
                 HB_CHECK(td_owner_counts(Ps[i], world, wper, Ps[i]->counts_dev.as<int64_t>(), st));
